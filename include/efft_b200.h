@@ -1,0 +1,95 @@
+/*
+ * efft_b200.h -- C ABI of the B200 large-1D-FFT library (libefft_b200.so).
+ *
+ * Plain pointers and sizes only; no C++ exception crosses this boundary and no
+ * torch type appears in a signature.  Every function returns an int status
+ * (EFFT_OK == 0); efft_last_error() gives a thread-local message.
+ *
+ * Each entry point replaces a reference interface of the Python package
+ * /root/reference/pkg/src/efft (cited file:line):
+ *
+ *   efft_plan_create      <- plan_create(n, splits, workers, test_mode, ...)   core.py:63-111
+ *                            + handle_create(plan) buffer/state set-up         core.py:126-144, 184-186
+ *   efft_execute          <- run_transform(handle) / TransformHandle.run()     recombine.py:298-308, core.py:166-170
+ *                            (device buffers, enqueued on the caller's stream)
+ *   efft_execute_host     <- the same call with host buffers: H2D copy, the two
+ *                            passes, D2H copy (what `handle.data[:] = x;
+ *                            run_transform(h); h.result` does end to end)
+ *   efft_plan_destroy     <- TransformHandle.close()                          core.py:172-174
+ *   efft_nonfinite_seen   <- scatter()'s non-finite input check               scatter.py:38-39
+ *   efft_last_error       <- the exception message of errors.py:4-45
+ *
+ * Status codes map 1:1 onto the reference exception classes (errors.py).
+ */
+#ifndef EFFT_B200_H
+#define EFFT_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define EFFT_OK 0
+#define EFFT_ERR_INVALID_ARG 1    /* ValueError                core.py:78-85        */
+#define EFFT_ERR_SPLITS_TOO_LARGE 2 /* SplitsTooLarge          core.py:87-89        */
+#define EFFT_ERR_SIZE_CONSTRAINT 3 /* SizeConstraintViolation core.py:90-94        */
+#define EFFT_ERR_UNSUPPORTED_SIZE 4 /* BinsizeNotPowerOfTwo    core.py:95-100 (here: N not M*2^t, M in {1,3}) */
+#define EFFT_ERR_ALLOC 5          /* AllocationFailure         memory.py:51-54      */
+#define EFFT_ERR_SIZE_MISMATCH 6  /* SizeMismatch              scatter.py:34-37     */
+#define EFFT_ERR_NONFINITE 7      /* ValueError (non-finite)   scatter.py:38-39     */
+#define EFFT_ERR_CUDA 8           /* CUDA runtime failure                           */
+#define EFFT_ERR_NCCL 9           /* collective failure (sharded path)              */
+
+#define EFFT_C64 1   /* complex64  (float2)  */
+#define EFFT_C128 2  /* complex128 (double2) */
+#define EFFT_R32 3   /* real float32 input, reference PERM-packed output
+                        [R_0, R_{n/2}, R_1, I_1, ...] (core.py:10-15), forward only */
+
+#define EFFT_FORWARD (-1) /* unnormalised exp(-2 pi i k n / N) (oracle.py:1-8)  */
+#define EFFT_INVERSE (+1) /* exp(+2 pi i k n / N), scaled by 1/N               */
+
+/* flags for efft_plan_create */
+#define EFFT_FLAG_CHECK_FINITE 0x1u /* detect non-finite input inside pass 1 */
+
+typedef struct efft_plan_s *efft_plan_t;
+
+/* Plan one forward or inverse transform of n complex elements on `device`.
+ * n must be M*2^t with M in {1,3}; allocates the staging ring and counters.
+ * The input buffer passed to efft_execute is never written; the output buffer
+ * doubles as the pass-1 intermediate (out-of-place, two device arrays). */
+int efft_plan_create(efft_plan_t *plan, int64_t n, int dtype, int direction, int device,
+                     uint32_t flags);
+
+/* Human-readable decomposition (passes, radices, tiles, grid). */
+int efft_plan_describe(efft_plan_t plan, char *buf, size_t len);
+
+/* Device workspace owned by the plan (staging ring + counters), bytes. */
+int efft_plan_workspace_bytes(efft_plan_t plan, size_t *bytes);
+
+/* Number of kernel launches one efft_execute enqueues. */
+int efft_plan_launches(efft_plan_t plan, int *launches);
+
+/* Enqueue the transform on `stream` (cudaStream_t, NULL = legacy default).
+ * d_in: n elements (read only); d_out: n elements.  Asynchronous. */
+int efft_execute(efft_plan_t plan, const void *d_in, void *d_out, void *stream);
+
+/* End-to-end call with HOST buffers (pinned or pageable): copies h_in to a
+ * plan-owned device input, runs efft_execute, copies the result to h_out and
+ * synchronises the stream. */
+int efft_execute_host(efft_plan_t plan, const void *h_in, void *h_out, void *stream);
+
+/* Returns (synchronising) whether any non-finite input value was seen by
+ * executions since the last call, and clears the flag. */
+int efft_nonfinite_seen(efft_plan_t plan, int *seen, void *stream);
+
+int efft_plan_destroy(efft_plan_t plan);
+
+const char *efft_last_error(void);
+int efft_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* EFFT_B200_H */

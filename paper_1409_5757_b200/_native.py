@@ -1,0 +1,143 @@
+"""ctypes binding of the C ABI in include/efft_b200.h (libefft_b200.so).
+
+The library is built in-tree by ``__graft_entry__.build()`` (csrc/Makefile).
+There is no CPU fallback: if the library is missing every transform raises
+``NativeLibraryMissing``.
+"""
+
+import ctypes
+import os
+
+from . import errors
+
+LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libefft_b200.so")
+
+EFFT_OK = 0
+EFFT_C64 = 1
+EFFT_C128 = 2
+EFFT_R32 = 3
+EFFT_FORWARD = -1
+EFFT_INVERSE = 1
+EFFT_FLAG_CHECK_FINITE = 0x1
+
+# status code -> exception class (include/efft_b200.h, reference errors.py)
+_STATUS = {
+    1: ValueError,
+    2: errors.SplitsTooLarge,
+    3: errors.SizeConstraintViolation,
+    4: errors.BinsizeNotPowerOfTwo,
+    5: errors.AllocationFailure,
+    6: errors.SizeMismatch,
+    7: ValueError,
+    8: errors.DeviceError,
+    9: errors.DeviceError,
+}
+
+# every symbol the header declares
+EXPORTED = (
+    "efft_plan_create",
+    "efft_plan_describe",
+    "efft_plan_workspace_bytes",
+    "efft_plan_launches",
+    "efft_execute",
+    "efft_execute_host",
+    "efft_nonfinite_seen",
+    "efft_plan_destroy",
+    "efft_last_error",
+    "efft_version",
+)
+
+_lib = None
+
+
+def load():
+    """Load libefft_b200.so once (no GPU needed to load)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise errors.NativeLibraryMissing(
+            f"{LIB_PATH} is not built; run __graft_entry__.build() (no CPU fallback exists)")
+    try:
+        lib = ctypes.CDLL(LIB_PATH)
+    except OSError as exc:
+        raise errors.NativeLibraryMissing(f"cannot load {LIB_PATH}: {exc}") from exc
+    vp, i32, i64, u32, sz = (ctypes.c_void_p, ctypes.c_int, ctypes.c_int64, ctypes.c_uint32,
+                             ctypes.c_size_t)
+    lib.efft_plan_create.argtypes = [ctypes.POINTER(vp), i64, i32, i32, i32, u32]
+    lib.efft_plan_describe.argtypes = [vp, ctypes.c_char_p, sz]
+    lib.efft_plan_workspace_bytes.argtypes = [vp, ctypes.POINTER(sz)]
+    lib.efft_plan_launches.argtypes = [vp, ctypes.POINTER(i32)]
+    lib.efft_execute.argtypes = [vp, vp, vp, vp]
+    lib.efft_execute_host.argtypes = [vp, vp, vp, vp]
+    lib.efft_nonfinite_seen.argtypes = [vp, ctypes.POINTER(i32), vp]
+    lib.efft_plan_destroy.argtypes = [vp]
+    lib.efft_last_error.restype = ctypes.c_char_p
+    lib.efft_last_error.argtypes = []
+    lib.efft_version.argtypes = []
+    for name in EXPORTED:
+        if name not in ("efft_last_error",):
+            getattr(lib, name).restype = i32
+    _lib = lib
+    return lib
+
+
+def check(rc: int, what: str = "") -> None:
+    if rc == EFFT_OK:
+        return
+    msg = load().efft_last_error().decode(errors="replace")
+    exc = _STATUS.get(rc, errors.DeviceError)
+    raise exc(f"{what}: {msg}" if what else msg)
+
+
+class NativePlan:
+    """Owns one efft_plan_t."""
+
+    def __init__(self, n: int, dtype: int, direction: int, device: int, flags: int = 0):
+        lib = load()
+        h = ctypes.c_void_p()
+        check(lib.efft_plan_create(ctypes.byref(h), n, dtype, direction, device, flags),
+              "efft_plan_create")
+        self._h = h
+        self.n, self.dtype, self.direction, self.device = n, dtype, direction, device
+
+    @property
+    def handle(self):
+        return self._h
+
+    def describe(self) -> str:
+        buf = ctypes.create_string_buffer(4096)
+        check(load().efft_plan_describe(self._h, buf, 4096))
+        return buf.value.decode()
+
+    def workspace_bytes(self) -> int:
+        v = ctypes.c_size_t()
+        check(load().efft_plan_workspace_bytes(self._h, ctypes.byref(v)))
+        return v.value
+
+    def launches(self) -> int:
+        v = ctypes.c_int()
+        check(load().efft_plan_launches(self._h, ctypes.byref(v)))
+        return v.value
+
+    def execute(self, d_in: int, d_out: int, stream: int) -> None:
+        check(load().efft_execute(self._h, d_in, d_out, stream), "efft_execute")
+
+    def execute_host(self, h_in: int, h_out: int, stream: int) -> None:
+        check(load().efft_execute_host(self._h, h_in, h_out, stream), "efft_execute_host")
+
+    def nonfinite_seen(self, stream: int) -> bool:
+        v = ctypes.c_int()
+        check(load().efft_nonfinite_seen(self._h, ctypes.byref(v), stream))
+        return bool(v.value)
+
+    def close(self) -> None:
+        if self._h:
+            load().efft_plan_destroy(self._h)
+            self._h = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

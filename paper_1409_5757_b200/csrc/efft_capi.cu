@@ -1,0 +1,547 @@
+// efft_capi.cu -- planner, executor and the C ABI (include/efft_b200.h).
+//
+// Planner (reference counterpart: plan_create, core.py:63-111).  N = M * 2^t,
+// M in {1, 3}, is split into at most two Stockham passes N = R1 * R2 (the
+// four-step form of the reference's scatter -> leaves -> merges).  A pass whose
+// radix fits one tile (<= 512 points, <= 384 with the factor 3) is "direct";
+// a larger one is "staged" as R = rho_a * rho_b through the L2 staging ring.
+//
+// Executor (reference counterpart: run_transform, recombine.py:298-308): one
+// memset of the task counters, then one persistent kernel launch per pass,
+// all on the caller's stream.  Pass 1 reads `in` and writes `out`; pass 2 runs
+// in place on `out` (its tiles read every element they write before writing),
+// so the input is preserved (core.py:146-149) with just two device arrays.
+#include <cuda_runtime.h>
+
+#include <cstdarg>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <string>
+
+#include "../../include/efft_b200.h"
+#include "efft_registry.cuh"
+
+using efft::KernelInfo;
+using efft::PassArgs;
+using efft::SubDesc;
+
+namespace {
+
+// Real-input post-process (reference leaf_dft.py:113-125, in place over the
+// half-length complex spectrum Z of the n/2 pairs):
+//   F_k = Z_k P_k + conj(Z_{h-k}) Q_k,  P_k = 1/2 - i/2 w^k,  Q_k = 1/2 + i/2 w^k,
+//   w = exp(-2 pi i / n); packed as [F_0, F_{n/2}, Re F_1, Im F_1, ...].
+// Thread k in [0, h/2] owns the pair (k, h-k) so the update is in place.
+__global__ void real_split_kernel(float2* z, int64_t h, int64_t n) {
+  const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (k > h / 2) return;
+  if (k == 0) {
+    const float2 z0 = z[0];
+    z[0] = make_float2(z0.x + z0.y, z0.x - z0.y);
+    if (h > 1 && (h & 1) == 0) {  // k = h/2 is self-paired: F = conj(Z)
+      const float2 zm = z[h / 2];
+      z[h / 2] = make_float2(zm.x, -zm.y);
+    }
+    return;
+  }
+  if (2 * k == h) return;  // handled by k == 0
+  const int64_t kk = h - k;
+  const float2 a = z[k], b = z[kk];
+  double s1, c1, s2, c2;
+  sincospi(-2.0 * (double)k / (double)n, &s1, &c1);
+  sincospi(-2.0 * (double)kk / (double)n, &s2, &c2);
+  // F_k with w^k = (c1, s1): P = (1/2 + s1/2, -c1/2), Q = (1/2 - s1/2, c1/2)
+  auto out = [](float2 zk, float2 zr, double c, double s) {
+    const double pr = 0.5 + 0.5 * s, pi = -0.5 * c, qr = 0.5 - 0.5 * s, qi = 0.5 * c;
+    const double cr = zr.x, ci = -zr.y;  // conj(Z_{h-k})
+    return make_float2((float)(zk.x * pr - zk.y * pi + cr * qr - ci * qi),
+                       (float)(zk.x * pi + zk.y * pr + cr * qi + ci * qr));
+  };
+  const float2 fk = out(a, b, c1, s1);
+  const float2 fkk = out(b, a, c2, s2);
+  z[k] = fk;
+  z[kk] = fkk;
+}
+
+thread_local std::string g_err;
+
+int fail(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+#define CUDA_TRY(x)                                                                    \
+  do {                                                                                 \
+    cudaError_t e_ = (x);                                                              \
+    if (e_ != cudaSuccess) return fail(EFFT_ERR_CUDA, "%s: %s", #x, cudaGetErrorString(e_)); \
+  } while (0)
+
+struct PassPlan {
+  KernelInfo k;
+  PassArgs args;
+  int grid;
+  int64_t radix, rho_a, rho_b;
+  int64_t counter_off;  // offset (in int32 units) of this pass's counters
+  int64_t counter_len;
+  bool staged;
+};
+
+}  // namespace
+
+struct efft_plan_s {
+  int64_t n;        // complex length the passes run on (n_user / 2 for EFFT_R32)
+  int64_t n_user;
+  bool real_input = false;
+  int dtype, direction, device;
+  uint32_t flags;
+  int npass;
+  PassPlan pass[2];
+  size_t elem;
+  void* staging = nullptr;
+  size_t staging_bytes = 0;
+  int32_t* counters = nullptr;
+  size_t counter_bytes = 0;
+  int32_t* flag = nullptr;
+  void* h_dev_in = nullptr;  // lazily allocated for efft_execute_host
+  void* h_dev_out = nullptr;
+  int num_sms = 0;
+};
+
+namespace {
+
+bool factor(int64_t n, int* M, int* t) {
+  if (n < 1) return false;
+  int tt = 0;
+  while ((n & 1) == 0) {
+    n >>= 1;
+    ++tt;
+  }
+  if (n != 1 && n != 3) return false;
+  *M = (int)n;
+  *t = tt;
+  return true;
+}
+
+bool get_direct(int dtype, int rho, KernelInfo* k) {
+  return dtype == EFFT_C64 ? efft::get_direct_kernel_f32(rho, k) : efft::get_direct_kernel_f64(rho, k);
+}
+bool get_staged(int dtype, int ra, int rb, KernelInfo* k) {
+  return dtype == EFFT_C64 ? efft::get_staged_kernel_f32(ra, rb, k)
+                           : efft::get_staged_kernel_f64(ra, rb, k);
+}
+
+int env_int(const char* name, int dflt) {
+  const char* v = getenv(name);
+  return v && *v ? atoi(v) : dflt;
+}
+
+// Decide direct vs staged and the sub-radices of one pass of radix R.
+bool pick_pass(int dtype, int64_t R, PassPlan* pp) {
+  pp->radix = R;
+  const bool has3 = (R % 3) == 0;
+  const int64_t dmax = has3 ? 384 : 512;
+  if (R <= dmax) {
+    pp->staged = false;
+    pp->rho_a = R;
+    pp->rho_b = 0;
+    return get_direct(dtype, (int)R, &pp->k);
+  }
+  pp->staged = true;
+  pp->rho_a = has3 ? 384 : 512;
+  pp->rho_b = R / pp->rho_a;
+  if (pp->rho_b * pp->rho_a != R) return false;
+  // B tiles cover D = 512/rho_b outputs of the rho_a-point DFTs: D | rho_a
+  if (pp->rho_a % (512 / pp->rho_b) != 0) return false;
+  return get_staged(dtype, (int)pp->rho_a, (int)pp->rho_b, &pp->k);
+}
+
+SubDesc blank_desc() {
+  SubDesc d;
+  memset(&d, 0, sizeof d);
+  d.scale = 1.0;
+  d.ntasks = 1;
+  return d;
+}
+
+// Fill the descriptors of pass `p` (0-based) of `np` for a Stockham pass with
+// radix R and Ns = product of earlier radices.
+void describe_pass(efft_plan_s* pl, int p, int np, int64_t R, int64_t Ns) {
+  PassPlan& pp = pl->pass[p];
+  const int64_t N = pl->n;
+  const int64_t C = N / R;                     // columns j of this pass
+  const int F = pl->dtype == EFFT_C64 ? 16 : 8;  // 128-byte column runs
+  const bool first = p == 0, last = p == np - 1;
+  const bool inverse = pl->direction == EFFT_INVERSE;
+  PassArgs& a = pp.args;
+  memset(&a, 0, sizeof a);
+  a.a = blank_desc();
+  a.b = blank_desc();
+  if (!pp.staged) {
+    const int64_t D = pp.k.d_a;
+    SubDesc& d = a.a;
+    d.ncols = C;
+    d.cg = D * F;
+    d.cs = F;
+    d.ig = D * F;
+    d.if_ = 1;
+    d.is = F;
+    d.im = C;
+    if (Ns == 1) {  // out[j*R + r]: transposed, unit stride along r
+      d.og = D * F * R;
+      d.of = R;
+      d.os = F * R;
+      d.om = 1;
+      d.store_mode = 2;
+    } else {  // Ns == C: out[j + r*C], j-runs
+      d.og = D * F;
+      d.of = 1;
+      d.os = F;
+      d.om = C;
+      d.store_mode = 0;
+      d.tw_mod = N;  // W_N^(j*r)
+      d.Ag = D * F;
+      d.As = F;
+      d.Af = 1;
+      d.Cm = 1;
+    }
+    d.conj_in = first && inverse;
+    d.check_finite = first && (pl->flags & EFFT_FLAG_CHECK_FINITE);
+    d.conj_out = last && inverse;
+    d.scale = (last && inverse) ? 1.0 / (double)N : 1.0;
+    d.ntasks = 1;
+    a.ngroups = (C + D * F - 1) / (D * F);
+    a.total_tasks = a.ngroups;
+    a.staged = 0;
+    return;
+  }
+  const int64_t ra = pp.rho_a, rb = pp.rho_b;
+  const int64_t DB = pp.k.d_b;
+  SubDesc& A = a.a;
+  SubDesc& B = a.b;
+  // A: rows r = u + t*rb (task = u), rho_a-point DFT over t, into staging
+  A.ncols = C;
+  A.cg = F;
+  A.ig = F;
+  A.it = C;
+  A.if_ = 1;
+  A.im = rb * C;
+  if (Ns != 1) {
+    A.tw_mod = N;  // W_N^(j*r), j = grp*F + f, r = u + t*rb
+    A.Ag = F;
+    A.Af = 1;
+    A.Ct = 1;
+    A.Cm = rb;
+  }
+  A.out_staging = 1;
+  A.ot = ra * F;  // staging (u*ra + k1)*F + f
+  A.of = 1;
+  A.om = F;
+  A.store_mode = 0;
+  A.ntasks = (int32_t)rb;
+  A.conj_in = first && inverse;
+  A.check_finite = first && (pl->flags & EFFT_FLAG_CHECK_FINITE);
+  // B: k1 = task*DB + s, rho_b-point DFT over u with W_R^(k1*u)
+  B.ncols = C;
+  B.cg = F;
+  B.in_staging = 1;
+  B.it = DB * F;
+  B.is = F;
+  B.if_ = 1;
+  B.im = ra * F;
+  B.tw_mod = R;
+  B.At = DB;
+  B.As = 1;
+  B.Cm = 1;
+  if (Ns == 1) {  // out[j*R + k1 + ra*k2]: runs along k1 (s)
+    B.og = F * R;
+    B.of = R;
+    B.ot = DB;
+    B.os = 1;
+    B.om = ra;
+    B.store_mode = 1;
+  } else {  // out[j + (k1 + ra*k2)*C]
+    B.og = F;
+    B.of = 1;
+    B.ot = DB * C;
+    B.os = C;
+    B.om = ra * C;
+    B.store_mode = 0;
+  }
+  B.ntasks = (int32_t)(ra / DB);
+  B.conj_out = last && inverse;
+  B.scale = (last && inverse) ? 1.0 / (double)N : 1.0;
+  a.ngroups = C / F;
+  a.slot_elems = (int64_t)F * R;
+  a.staged = 1;
+  a.total_tasks = a.ngroups * (A.ntasks + B.ntasks);
+}
+
+int build_plan(efft_plan_s* pl) {
+  int M, t;
+  if (!factor(pl->n, &M, &t) || pl->n < 2)
+    return fail(EFFT_ERR_UNSUPPORTED_SIZE,
+                "n=%lld is not M*2^t with M in {1,3} and n >= 2", (long long)pl->n);
+  const int dt = pl->dtype;
+  int64_t R1, R2;
+  const int64_t dmax = M == 3 ? 384 : 512;
+  if (pl->n <= dmax) {
+    pl->npass = 1;
+    R1 = pl->n;
+    R2 = 1;
+  } else {
+    pl->npass = 2;
+    // balanced split; the factor 3 goes to pass 1
+    int t1 = t / 2;
+    R1 = (int64_t)M << t1;
+    R2 = pl->n / R1;
+    PassPlan a, b;
+    if (!pick_pass(dt, R1, &a) || !pick_pass(dt, R2, &b)) {
+      // shift one power of two between the passes and retry
+      bool ok = false;
+      for (int d : {-1, 1, -2, 2}) {
+        const int tt = t1 + d;
+        if (tt < 0 || tt > t) continue;
+        R1 = (int64_t)M << tt;
+        R2 = pl->n / R1;
+        if (pick_pass(dt, R1, &a) && pick_pass(dt, R2, &b)) {
+          ok = true;
+          break;
+        }
+      }
+      if (!ok) return fail(EFFT_ERR_UNSUPPORTED_SIZE, "no decomposition for n=%lld", (long long)pl->n);
+    }
+    // staged passes need >= F columns
+    const int F = dt == EFFT_C64 ? 16 : 8;
+    if ((a.staged && (pl->n / R1) % F) || (b.staged && (pl->n / R2) % F))
+      return fail(EFFT_ERR_UNSUPPORTED_SIZE, "n=%lld too small for its decomposition", (long long)pl->n);
+  }
+  const int64_t radices[2] = {R1, R2};
+  int64_t ns = 1;
+  int64_t coff = 2;  // int32 units; [0,2) = 64-bit task counter of pass 0
+  size_t staging_bytes = 0;
+  for (int p = 0; p < pl->npass; ++p) {
+    PassPlan& pp = pl->pass[p];
+    if (!pick_pass(dt, radices[p], &pp))
+      return fail(EFFT_ERR_UNSUPPORTED_SIZE, "no kernel for radix %lld", (long long)radices[p]);
+    describe_pass(pl, p, pl->npass, radices[p], ns);
+    ns *= radices[p];
+    CUDA_TRY(cudaFuncSetAttribute(pp.k.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, pp.k.smem_bytes));
+    int occ = 0;
+    CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, pp.k.fn, pp.k.nt, pp.k.smem_bytes));
+    if (occ < 1) return fail(EFFT_ERR_CUDA, "kernel does not fit on an SM (smem %d)", pp.k.smem_bytes);
+    int64_t grid = (int64_t)occ * pl->num_sms;
+    if (grid > pp.args.total_tasks) grid = pp.args.total_tasks;
+    pp.grid = (int)grid;
+    PassArgs& a = pp.args;
+    if (pp.staged) {
+      const int64_t per = a.a.ntasks + a.b.ntasks;
+      int64_t lag = (grid + per - 1) / per + 1;
+      lag = env_int("EFFT_LAG", (int)lag);
+      if (lag < 1) lag = 1;
+      if (lag > a.ngroups) lag = a.ngroups;
+      int64_t slots = env_int("EFFT_SLOTS", (int)(lag + 2));
+      if (slots < lag + 1) slots = lag + 1;
+      if (slots > a.ngroups) slots = a.ngroups;
+      a.lag = (int32_t)lag;
+      a.nslots = (int32_t)slots;
+      size_t sb = (size_t)slots * a.slot_elems * pl->elem;
+      if (sb > staging_bytes) staging_bytes = sb;
+      pp.counter_off = coff;
+      pp.counter_len = 2 + 2 * a.ngroups;
+    } else {
+      pp.counter_off = coff;
+      pp.counter_len = 2;
+    }
+    coff += pp.counter_len;
+  }
+  pl->staging_bytes = staging_bytes;
+  pl->counter_bytes = (size_t)coff * 4;
+  return EFFT_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int efft_version(void) { return 1; }
+
+const char* efft_last_error(void) { return g_err.c_str(); }
+
+int efft_plan_create(efft_plan_t* out, int64_t n, int dtype, int direction, int device,
+                     uint32_t flags) {
+  if (!out) return fail(EFFT_ERR_INVALID_ARG, "plan pointer is NULL");
+  *out = nullptr;
+  if (dtype != EFFT_C64 && dtype != EFFT_C128 && dtype != EFFT_R32)
+    return fail(EFFT_ERR_INVALID_ARG, "dtype %d", dtype);
+  if (dtype == EFFT_R32 && direction != EFFT_FORWARD)
+    return fail(EFFT_ERR_INVALID_ARG, "the real-input path is forward only");
+  if (dtype == EFFT_R32 && (n < 4 || (n & 1)))
+    return fail(EFFT_ERR_UNSUPPORTED_SIZE, "real-input n must be even and >= 4, got %lld", (long long)n);
+  if (direction != EFFT_FORWARD && direction != EFFT_INVERSE)
+    return fail(EFFT_ERR_INVALID_ARG, "direction must be -1 or +1, got %d", direction);
+  if (n < 1) return fail(EFFT_ERR_INVALID_ARG, "n must be >= 1");
+  int ndev = 0;
+  CUDA_TRY(cudaGetDeviceCount(&ndev));
+  if (device < 0 || device >= ndev) return fail(EFFT_ERR_INVALID_ARG, "device %d of %d", device, ndev);
+  CUDA_TRY(cudaSetDevice(device));
+  efft_plan_s* pl = new efft_plan_s();
+  pl->n_user = n;
+  pl->real_input = dtype == EFFT_R32;
+  pl->n = pl->real_input ? n / 2 : n;
+  if (pl->real_input) dtype = EFFT_C64;
+  pl->dtype = dtype;
+  pl->direction = direction;
+  pl->device = device;
+  pl->flags = flags;
+  pl->elem = dtype == EFFT_C64 ? 8 : 16;
+  cudaDeviceGetAttribute(&pl->num_sms, cudaDevAttrMultiProcessorCount, device);
+  int rc = build_plan(pl);
+  if (rc == EFFT_OK && pl->staging_bytes) {
+    if (cudaMalloc(&pl->staging, pl->staging_bytes) != cudaSuccess) {
+      cudaGetLastError();
+      rc = fail(EFFT_ERR_ALLOC, "staging ring of %zu bytes", pl->staging_bytes);
+    }
+  }
+  if (rc == EFFT_OK && cudaMalloc((void**)&pl->counters, pl->counter_bytes) != cudaSuccess) {
+    cudaGetLastError();
+    rc = fail(EFFT_ERR_ALLOC, "counters");
+  }
+  if (rc == EFFT_OK && cudaMalloc((void**)&pl->flag, 4) != cudaSuccess) {
+    cudaGetLastError();
+    rc = fail(EFFT_ERR_ALLOC, "flag");
+  }
+  if (rc == EFFT_OK && cudaMemset(pl->flag, 0, 4) != cudaSuccess) rc = fail(EFFT_ERR_CUDA, "memset flag");
+  if (rc != EFFT_OK) {
+    std::string keep = g_err;
+    efft_plan_destroy(pl);
+    g_err = keep;
+    return rc;
+  }
+  for (int p = 0; p < pl->npass; ++p) {
+    PassArgs& a = pl->pass[p].args;
+    a.staging = pl->staging;
+    a.task_counter = reinterpret_cast<unsigned long long*>(pl->counters + pl->pass[p].counter_off);
+    a.doneA = pl->counters + pl->pass[p].counter_off + 2;
+    a.doneB = a.doneA + a.ngroups;
+    a.flag = pl->flag;
+  }
+  *out = pl;
+  return EFFT_OK;
+}
+
+int efft_plan_describe(efft_plan_t pl, char* buf, size_t len) {
+  if (!pl || !buf) return fail(EFFT_ERR_INVALID_ARG, "NULL argument");
+  std::string s;
+  char line[512];
+  snprintf(line, sizeof line, "n=%lld dtype=%s direction=%d passes=%d staging=%zu B\n",
+           (long long)pl->n, pl->dtype == EFFT_C64 ? "c64" : "c128", pl->direction, pl->npass,
+           pl->staging_bytes);
+  s += line;
+  for (int p = 0; p < pl->npass; ++p) {
+    const PassPlan& pp = pl->pass[p];
+    std::string st;
+    for (int i = 0; i < pp.k.nst_a; ++i) st += (i ? "x" : "") + std::to_string(pp.k.stages_a[i]);
+    if (pp.staged) {
+      st += " | ";
+      for (int i = 0; i < pp.k.nst_b; ++i) st += (i ? "x" : "") + std::to_string(pp.k.stages_b[i]);
+    }
+    snprintf(line, sizeof line,
+             "pass %d: R=%lld %s rho_a=%lld rho_b=%lld stages=[%s] grid=%d x %d smem=%d groups=%lld "
+             "tasks=%lld lag=%d slots=%d\n",
+             p, (long long)pp.radix, pp.staged ? "staged" : "direct", (long long)pp.rho_a,
+             (long long)pp.rho_b, st.c_str(), pp.grid, pp.k.nt, pp.k.smem_bytes,
+             (long long)pp.args.ngroups, (long long)pp.args.total_tasks, pp.args.lag, pp.args.nslots);
+    s += line;
+  }
+  snprintf(buf, len, "%s", s.c_str());
+  return EFFT_OK;
+}
+
+int efft_plan_workspace_bytes(efft_plan_t pl, size_t* bytes) {
+  if (!pl || !bytes) return fail(EFFT_ERR_INVALID_ARG, "NULL argument");
+  *bytes = pl->staging_bytes + pl->counter_bytes + 4;
+  return EFFT_OK;
+}
+
+int efft_plan_launches(efft_plan_t pl, int* launches) {
+  if (!pl || !launches) return fail(EFFT_ERR_INVALID_ARG, "NULL argument");
+  *launches = pl->npass + (pl->real_input ? 1 : 0);
+  return EFFT_OK;
+}
+
+int efft_execute(efft_plan_t pl, const void* d_in, void* d_out, void* stream) {
+  if (!pl || !d_in || !d_out) return fail(EFFT_ERR_INVALID_ARG, "NULL argument");
+  if (d_in == d_out) return fail(EFFT_ERR_INVALID_ARG, "in-place execution is not supported");
+  const size_t bytes = (size_t)pl->n * pl->elem;
+  const char* i0 = (const char*)d_in;
+  const char* o0 = (const char*)d_out;
+  if (i0 < o0 + bytes && o0 < i0 + bytes) return fail(EFFT_ERR_INVALID_ARG, "input and output overlap");
+  cudaStream_t s = (cudaStream_t)stream;
+  CUDA_TRY(cudaSetDevice(pl->device));
+  CUDA_TRY(cudaMemsetAsync(pl->counters, 0, pl->counter_bytes, s));
+  for (int p = 0; p < pl->npass; ++p) {
+    PassArgs a = pl->pass[p].args;
+    a.in = p == 0 ? d_in : d_out;
+    a.out = d_out;
+    const PassPlan& pp = pl->pass[p];
+    pp.k.fn<<<pp.grid, pp.k.nt, pp.k.smem_bytes, s>>>(a);
+    CUDA_TRY(cudaGetLastError());
+  }
+  if (pl->real_input) {
+    const int64_t h = pl->n, work = h / 2 + 1;
+    real_split_kernel<<<(unsigned)((work + 255) / 256), 256, 0, s>>>((float2*)d_out, h, pl->n_user);
+    CUDA_TRY(cudaGetLastError());
+  }
+  return EFFT_OK;
+}
+
+int efft_execute_host(efft_plan_t pl, const void* h_in, void* h_out, void* stream) {
+  if (!pl || !h_in || !h_out) return fail(EFFT_ERR_INVALID_ARG, "NULL argument");
+  CUDA_TRY(cudaSetDevice(pl->device));
+  const size_t bytes = (size_t)pl->n * pl->elem;
+  if (!pl->h_dev_in) {
+    if (cudaMalloc(&pl->h_dev_in, bytes) != cudaSuccess || cudaMalloc(&pl->h_dev_out, bytes) != cudaSuccess) {
+      cudaGetLastError();
+      return fail(EFFT_ERR_ALLOC, "device buffers for host execution (%zu bytes each)", bytes);
+    }
+  }
+  cudaStream_t s = (cudaStream_t)stream;
+  CUDA_TRY(cudaMemcpyAsync(pl->h_dev_in, h_in, bytes, cudaMemcpyHostToDevice, s));
+  int rc = efft_execute(pl, pl->h_dev_in, pl->h_dev_out, stream);
+  if (rc != EFFT_OK) return rc;
+  CUDA_TRY(cudaMemcpyAsync(h_out, pl->h_dev_out, bytes, cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(cudaStreamSynchronize(s));
+  return EFFT_OK;
+}
+
+int efft_nonfinite_seen(efft_plan_t pl, int* seen, void* stream) {
+  if (!pl || !seen) return fail(EFFT_ERR_INVALID_ARG, "NULL argument");
+  CUDA_TRY(cudaSetDevice(pl->device));
+  cudaStream_t s = (cudaStream_t)stream;
+  int32_t v = 0;
+  CUDA_TRY(cudaMemcpyAsync(&v, pl->flag, 4, cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(cudaStreamSynchronize(s));
+  CUDA_TRY(cudaMemsetAsync(pl->flag, 0, 4, s));
+  *seen = v != 0;
+  return EFFT_OK;
+}
+
+int efft_plan_destroy(efft_plan_t pl) {
+  if (!pl) return EFFT_OK;
+  cudaSetDevice(pl->device);
+  if (pl->staging) cudaFree(pl->staging);
+  if (pl->counters) cudaFree(pl->counters);
+  if (pl->flag) cudaFree(pl->flag);
+  if (pl->h_dev_in) cudaFree(pl->h_dev_in);
+  if (pl->h_dev_out) cudaFree(pl->h_dev_out);
+  delete pl;
+  return EFFT_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,51 @@
+// efft_registry.cuh -- compiled tile/kernel variants the planner can pick from.
+#pragma once
+#include "efft_kernels.cuh"
+
+namespace efft {
+
+struct KernelInfo {
+  void (*fn)(PassArgs);
+  int nt;          // threads per CTA
+  int smem_bytes;  // dynamic shared memory
+  int rho_a, d_a, e_a;
+  int rho_b, d_b, e_b;
+  int stages_a[12], nst_a;
+  int stages_b[12], nst_b;
+};
+
+// Power-of-two tiles hold D*RHO = 512 points per column group, radix-3 tiles
+// 384; 256 threads; F columns of 128 bytes.
+template <typename R, int RHO> using PT = Tile<R, RHO, 512 / RHO, 256>;
+template <typename R, int RHO> using T3 = Tile<R, RHO, 384 / RHO, 256>;
+
+template <typename R, class TA, class TB>
+KernelInfo make_info() {
+  using V = typename CT<R>::V;
+  KernelInfo k{};
+  k.fn = pass_kernel<R, TA, TB>;
+  k.nt = TA::NT;
+  const int sm = TA::SMEM_ELEMS > TB::SMEM_ELEMS ? TA::SMEM_ELEMS : TB::SMEM_ELEMS;
+  k.smem_bytes = (int)((sm + TA::RHO + TB::RHO) * sizeof(V));
+  k.rho_a = TA::RHO;
+  k.d_a = TA::D;
+  k.e_a = TA::E;
+  k.nst_a = TA::NST;
+  for (int i = 0; i < TA::NST; ++i) k.stages_a[i] = TA::PL.sig[i];
+  if constexpr (TB::RHO > 0) {
+    k.rho_b = TB::RHO;
+    k.d_b = TB::D;
+    k.e_b = TB::E;
+    k.nst_b = TB::NST;
+    for (int i = 0; i < TB::NST; ++i) k.stages_b[i] = TB::PL.sig[i];
+  }
+  return k;
+}
+
+// Defined in inst_f32.cu / inst_f64.cu.
+bool get_direct_kernel_f32(int rho, KernelInfo* out);
+bool get_direct_kernel_f64(int rho, KernelInfo* out);
+bool get_staged_kernel_f32(int rho_a, int rho_b, KernelInfo* out);
+bool get_staged_kernel_f64(int rho_a, int rho_b, KernelInfo* out);
+
+}  // namespace efft

@@ -1,0 +1,34 @@
+// Explicit kernel variants for float data (see efft_registry.cuh).
+#include "efft_registry.cuh"
+
+namespace efft {
+
+#define D2(r) case r: *out = make_info<float, PT<float, r>, NoTile>(); return true;
+#define D3(r) case r: *out = make_info<float, T3<float, r>, NoTile>(); return true;
+bool get_direct_kernel_f32(int rho, KernelInfo* out) {
+  switch (rho) {
+    D2(2) D2(4) D2(8) D2(16) D2(32) D2(64) D2(128) D2(256) D2(512)
+    D3(3) D3(6) D3(12) D3(24) D3(48) D3(96) D3(192) D3(384)
+    default: return false;
+  }
+}
+#undef D2
+#undef D3
+
+#define SA(rb) case rb: *out = make_info<float, Tile<float, RA, 1, 256>, PT<float, rb>>(); return true;
+template <int RA>
+static bool staged_f32(int rho_b, KernelInfo* out) {
+  switch (rho_b) {
+    SA(2) SA(4) SA(8) SA(16) SA(32) SA(64) SA(128) SA(256) SA(512)
+    default: return false;
+  }
+}
+#undef SA
+
+bool get_staged_kernel_f32(int rho_a, int rho_b, KernelInfo* out) {
+  if (rho_a == 512) return staged_f32<512>(rho_b, out);
+  if (rho_a == 384) return staged_f32<384>(rho_b, out);
+  return false;
+}
+
+}  // namespace efft
