@@ -1,0 +1,370 @@
+#!/usr/bin/env python
+"""Benchmark: GFLOP/s (5*N*log2 N) and HBM GB/s of one large 1D FFT on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c3] [--impl ours|reference]
+
+Default workload (BASELINE.json metric, north-star target config): C3, a forward
+complex64 DFT of N = 2^30 (8 GiB), seeded N(0,1) synthetic input.  A "step" is one
+transform (C2/C5: one forward + one inverse transform).  The input (8 GiB) is far
+larger than the 126 MB L2, so no L2 flush is needed between steps; configs that fit
+in L2 (C1) are timed per step with an L2 flush between steps.
+
+Prints ONE JSON line (rank 0).  Keys beyond the base contract:
+  roofline      dominant kernel (a pass kernel): algorithmic bytes per launch
+                (2*N*sizeof(element): one read + one write of the array) over its
+                average CUDA-event duration, against MEASURED_PEAKS.json hbm_gbs
+  cpu_baseline  the CPU restatement of the reference algorithm (oracle/, float32
+                arithmetic with the reference's twiddle recipe for c64 configs, fp64
+                for c128) timed on the host cores on a bounded sample
+  e2e           the same metric through the C-ABI host-buffer entry
+                (efft_execute_host): pinned host in -> H2D -> passes -> D2H -> host out
+--impl reference times that CPU restatement (the reference itself is Python and
+cannot travel to the GPU box) and prints the same line shape.
+Multi-GPU (torchrun): each rank transforms its own array (replicas, weak scaling);
+the time is the max over ranks.
+"""
+import argparse
+import json
+import math
+import os
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+DTYPE_NAME = {"complex64": "f32", "complex128": "f64"}
+ELEM = {"complex64": 8, "complex128": 16}
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as fh:
+            d = json.load(fh)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """Samples SM clocks and throttle reasons with NVML during the timed region."""
+
+    NAMES = {
+        0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+        0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
+        0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+        0x100: "display_clock_setting",
+    }
+
+    def __init__(self, device_index):
+        self.samples, self.reasons, self.max_mhz = [], 0, None
+        self._stop = threading.Event()
+        self._t = None
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self._nv = pynvml
+            self._h = pynvml.nvmlDeviceGetHandleByIndex(device_index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self._h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self._nv = None
+
+    def _run(self):
+        nv = self._nv
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self._h, nv.NVML_CLOCK_SM))
+                self.reasons |= nv.nvmlDeviceGetCurrentClocksEventReasons(self._h)
+            except Exception:
+                pass
+            time.sleep(0.05)
+
+    def __enter__(self):
+        if self._nv:
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        if self._t:
+            self._t.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["nvml_unavailable"]}
+        s = sorted(self.samples)
+        names = [v for k, v in self.NAMES.items() if self.reasons & k and k != 0x1]
+        return {"sm_mhz": s[len(s) // 2], "sm_max_mhz": self.max_mhz, "reasons": names,
+                "samples": len(s)}
+
+
+def dist_init():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    return rank, local, world
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+
+
+def max_over_ranks(v, world):
+    if world == 1:
+        return v
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([v], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def cpu_baseline(cfg_name, cfg, x_dev, max_seconds=25.0):
+    """Time the oracle (CPU restatement of the reference algorithm) on a bounded sample."""
+    import numpy as np
+
+    import oracle
+
+    threads = oracle.host_threads()
+    prec = "c64" if cfg["dtype"] == "complex64" else "c128"
+    n_full = cfg["n"]
+    # bounded sample: the largest power-of-two prefix (x 3 for C4) that runs in ~max_seconds
+    m = 3 if n_full % 3 == 0 else 1
+    n = min(n_full, m << 22)
+    host = x_dev[:n_full].cpu().numpy() if n_full <= (1 << 30) else None
+    best = None
+    while True:
+        if host is not None:
+            x = np.ascontiguousarray(host[:n])
+        else:
+            x = x_dev[:n].cpu().numpy()
+        t0 = time.perf_counter()
+        oracle.transform(x, precision=prec, threads=threads)
+        dt = time.perf_counter() - t0
+        best = (n, dt)
+        if n >= n_full or dt * 2.3 > max_seconds:
+            break
+        n *= 2
+    n, dt = best
+    gflops = 5.0 * n * math.log2(n) / dt / 1e9
+    return {"value": round(gflops, 3), "unit": "GFLOP/s", "cores": threads, "kind": "port",
+            "sample": f"one {prec} transform of N={n} (prefix of {cfg_name}'s N={n_full} input), "
+                      f"{dt:.2f} s, oracle/efft_oracle.c with {threads} OpenMP threads"}
+
+
+def run_reference(args):
+    """--impl reference: the CPU restatement of the reference path, rank 0 only."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import numpy as np
+
+    import oracle
+    from paper_1409_5757_b200 import workloads
+
+    cfg = workloads.CONFIGS[args.config]
+    prec = "c64" if cfg["dtype"] == "complex64" else "c128"
+    threads = oracle.host_threads()
+    m = 3 if cfg["n"] % 3 == 0 else 1
+    n = min(cfg["n"], m << 24)  # bounded sample per step (~1-3 s on 16 cores)
+    rng = np.random.default_rng(workloads.seed_for(args.config))
+    x = (rng.standard_normal(n) + 1j * rng.standard_normal(n)).astype(
+        np.complex64 if prec == "c64" else np.complex128)
+    out = np.empty_like(x)
+    per_step = 2 if cfg["roundtrip"] else 1
+    for _ in range(args.warmup):
+        oracle.transform(x, precision=prec, threads=threads, out=out)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        for r in range(per_step):
+            oracle.transform(x if r == 0 else out, direction=-1 if r == 0 else 1, precision=prec,
+                             threads=threads, out=out if r == 0 else x)
+    dt = time.perf_counter() - t0
+    flops = 5.0 * n * math.log2(n) * per_step * args.steps
+    gflops = flops / dt / 1e9
+    line = {
+        "impl": "reference", "metric": "GFLOP/s (5N*log2N) per 1D FFT",
+        "value": round(gflops, 3), "unit": "GFLOP/s", "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(dt / args.steps * 1e3, 3),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": DTYPE_NAME[cfg["dtype"]], "data": "synthetic",
+        "config": {"workload": f"{args.config}: {cfg['dtype']} 1D DFT, N={cfg['n']}",
+                   "sample_n": n, "roundtrip": cfg["roundtrip"]},
+        "cpu_baseline": {"value": round(gflops, 3), "unit": "GFLOP/s", "cores": threads,
+                         "kind": "port",
+                         "sample": f"each step = {per_step} {prec} transform(s) of N={n} (bounded "
+                                   f"sample of N={cfg['n']}); oracle/efft_oracle.c, the C restatement "
+                                   f"of the reference EFFT algorithm (reference is Python-only)"},
+        "e2e": {"value": round(gflops, 3), "unit": "GFLOP/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args):
+    import torch
+
+    import paper_1409_5757_b200 as efft
+    from paper_1409_5757_b200 import _native, workloads
+
+    rank, local, world = dist_init()
+    torch.cuda.set_device(local)
+    cfg = workloads.CONFIGS[args.config]
+    n, dtype = cfg["n"], cfg["dtype"]
+    seed = workloads.seed_for(args.config) + rank
+    x = workloads.make_input(n, dtype, cfg["kind"], seed, device="cuda")
+    y = torch.empty_like(x)
+    ndt = _native.EFFT_C64 if dtype == "complex64" else _native.EFFT_C128
+    fwd = _native.NativePlan(n, ndt, -1, local)
+    inv = _native.NativePlan(n, ndt, 1, local) if cfg["roundtrip"] else None
+    fwd.enable_timing(True)
+    stream = torch.cuda.current_stream()
+    sid = stream.cuda_stream
+    per_step = 2 if cfg["roundtrip"] else 1
+    l2_resident = n * ELEM[dtype] * 2 <= 96 << 20
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda") if l2_resident else None
+
+    def step():
+        fwd.execute(x.data_ptr(), y.data_ptr(), sid)
+        if inv is not None:
+            inv.execute(y.data_ptr(), x.data_ptr(), sid)
+
+    for _ in range(max(args.warmup, 3)):
+        step()
+    torch.cuda.synchronize()
+    launches = fwd.launches() + (inv.launches() if inv else 0)
+    pass_ms = [[] for _ in range(fwd.launches())]
+    barrier(world)
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clocks:
+        if flush is None:
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            for i in range(args.steps):
+                step()
+                if i == args.steps - 1:
+                    pass
+            e1.record()
+            torch.cuda.synchronize()
+            total_ms = e0.elapsed_time(e1)
+            # per-launch durations of the last step (events on the launching stream)
+            for k, v in enumerate(fwd.launch_times_ms()):
+                pass_ms[k].append(v)
+        else:
+            total_ms = 0.0
+            for _ in range(args.steps):
+                flush.zero_()
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record()
+                step()
+                e1.record()
+                torch.cuda.synchronize()
+                total_ms += e0.elapsed_time(e1)
+                for k, v in enumerate(fwd.launch_times_ms()):
+                    pass_ms[k].append(v)
+    torch.cuda.synchronize()
+    barrier(world)
+    total_ms = max_over_ranks(total_ms, world)
+    ms_per_step = total_ms / args.steps
+    flops_per_transform = 5.0 * n * math.log2(n)
+    value = world * per_step * flops_per_transform * args.steps / (total_ms * 1e-3) / 1e9
+
+    # dominant kernel roofline (pass kernels move 2*N*elem algorithmic bytes each)
+    peak, peak_src = measured_peaks()
+    avg = [sum(v) / len(v) for v in pass_ms if v]
+    dom = max(range(len(avg)), key=lambda k: avg[k])
+    alg_bytes = 2 * n * ELEM[dtype]
+    achieved = alg_bytes / (avg[dom] * 1e-3) / 1e9
+    whole_gbs = per_step * fwd.launches() * alg_bytes / (ms_per_step * 1e-3) / 1e9
+
+    # e2e through the C-ABI host-buffer entry (rank-local), fewer steps: PCIe bound
+    e2e = None
+    if not args.no_e2e:
+        hin = torch.empty(n, dtype=x.dtype, pin_memory=True)
+        hout = torch.empty(n, dtype=x.dtype, pin_memory=True)
+        hin.copy_(x)
+        e2e_steps = max(1, min(args.steps, args.e2e_steps))
+        fwd.execute_host(hin.data_ptr(), hout.data_ptr(), sid)  # warm (allocates device buffers)
+        torch.cuda.synchronize()
+        barrier(world)
+        t0 = time.perf_counter()
+        for _ in range(e2e_steps):
+            fwd.execute_host(hin.data_ptr(), hout.data_ptr(), sid)
+            if inv is not None:
+                inv.execute_host(hout.data_ptr(), hin.data_ptr(), sid)
+        dt = max_over_ranks(time.perf_counter() - t0, world)
+        e2e = {"value": round(world * per_step * flops_per_transform * e2e_steps / dt / 1e9, 3),
+               "unit": "GFLOP/s",
+               "h2d_bytes_per_step": per_step * n * ELEM[dtype],
+               "d2h_bytes_per_step": per_step * n * ELEM[dtype],
+               "ms_per_step": round(dt / e2e_steps * 1e3, 3),
+               "path": "efft_execute_host (C ABI): pinned host -> H2D -> passes -> D2H -> host"}
+        del hin, hout
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        cpu = cpu_baseline(args.config, cfg, x)
+
+    if rank == 0:
+        line = {
+            "metric": "GFLOP/s (5N*log2N) per 1D FFT",
+            "value": round(value, 3), "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps,
+            "warmup": max(args.warmup, 3), "ms_per_step": round(ms_per_step, 4),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": DTYPE_NAME[dtype], "data": "synthetic (seeded torch generator, see workloads.py)",
+            "config": {"workload": f"{args.config}: {'forward+inverse' if cfg['roundtrip'] else 'forward'} "
+                                   f"1D {dtype} DFT, N={n}",
+                       "n": n, "input": cfg["kind"], "parallelism": f"replicas x{world}",
+                       "l2": "flushed between steps (512 MiB write)" if flush is not None
+                             else f"inputs ({n * ELEM[dtype] >> 20} MiB) larger than L2",
+                       "plan": fwd.describe().strip().splitlines()},
+            "hbm_gbs_whole_step": round(whole_gbs, 1),
+            "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
+                         "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": None,
+                         "kernel": f"pass {dom} (pass_kernel), {avg[dom]:.4f} ms avg",
+                         "pass_ms": [round(a, 4) for a in avg], "peak_source": peak_src,
+                         "alg_bytes_per_launch": alg_bytes},
+            "gpu_launches": launches * args.steps,
+            "clocks": clocks.summary(),
+            "e2e": e2e,
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="c3", choices=["c1", "c2", "c3", "c4", "c5"])
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--no-e2e", action="store_true", help="skip the host-buffer e2e leg")
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

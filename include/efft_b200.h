@@ -86,6 +86,13 @@ int efft_nonfinite_seen(efft_plan_t plan, int *seen, void *stream);
 
 int efft_plan_destroy(efft_plan_t plan);
 
+/* Per-launch device timing (CUDA events recorded on the execution stream
+ * around every kernel the plan launches).  Enable once; after an execution
+ * has completed, efft_plan_launch_times() fills ms[0..launches-1] with the
+ * durations of the most recent execution. */
+int efft_plan_enable_timing(efft_plan_t plan, int enable);
+int efft_plan_launch_times(efft_plan_t plan, float *ms, int max_launches);
+
 const char *efft_last_error(void);
 int efft_version(void);
 

@@ -43,6 +43,8 @@ EXPORTED = (
     "efft_execute_host",
     "efft_nonfinite_seen",
     "efft_plan_destroy",
+    "efft_plan_enable_timing",
+    "efft_plan_launch_times",
     "efft_last_error",
     "efft_version",
 )
@@ -72,6 +74,8 @@ def load():
     lib.efft_execute_host.argtypes = [vp, vp, vp, vp]
     lib.efft_nonfinite_seen.argtypes = [vp, ctypes.POINTER(i32), vp]
     lib.efft_plan_destroy.argtypes = [vp]
+    lib.efft_plan_enable_timing.argtypes = [vp, i32]
+    lib.efft_plan_launch_times.argtypes = [vp, ctypes.POINTER(ctypes.c_float), i32]
     lib.efft_last_error.restype = ctypes.c_char_p
     lib.efft_last_error.argtypes = []
     lib.efft_version.argtypes = []
@@ -130,6 +134,15 @@ class NativePlan:
         v = ctypes.c_int()
         check(load().efft_nonfinite_seen(self._h, ctypes.byref(v), stream))
         return bool(v.value)
+
+    def enable_timing(self, on: bool = True) -> None:
+        check(load().efft_plan_enable_timing(self._h, 1 if on else 0))
+
+    def launch_times_ms(self) -> list:
+        n = self.launches()
+        arr = (ctypes.c_float * n)()
+        check(load().efft_plan_launch_times(self._h, arr, n))
+        return list(arr)
 
     def close(self) -> None:
         if self._h:

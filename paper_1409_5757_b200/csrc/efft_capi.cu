@@ -111,6 +111,8 @@ struct efft_plan_s {
   void* h_dev_in = nullptr;  // lazily allocated for efft_execute_host
   void* h_dev_out = nullptr;
   int num_sms = 0;
+  bool timing = false;
+  cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};  // launch boundaries
 };
 
 namespace {
@@ -153,11 +155,14 @@ bool pick_pass(int dtype, int64_t R, PassPlan* pp) {
     return get_direct(dtype, (int)R, &pp->k);
   }
   pp->staged = true;
-  pp->rho_a = has3 ? 384 : 512;
+  pp->rho_a = has3 ? 384 : 256;
   pp->rho_b = R / pp->rho_a;
-  if (pp->rho_b * pp->rho_a != R) return false;
-  // B tiles cover D = 512/rho_b outputs of the rho_a-point DFTs: D | rho_a
-  if (pp->rho_a % (512 / pp->rho_b) != 0) return false;
+  if (pp->rho_b * pp->rho_a != R || pp->rho_b > 512) return false;
+  // A tiles take D_A = tile/rho_a consecutive u (D_A | rho_b); B tiles cover
+  // D_B = 512/rho_b outputs k1 of the rho_a-point DFTs (D_B | rho_a)
+  const int64_t tile = has3 ? 384 : 512;
+  const int64_t da = tile / pp->rho_a;
+  if (pp->rho_b % da != 0 || pp->rho_b > tile || pp->rho_a % (tile / pp->rho_b) != 0) return false;
   return get_staged(dtype, (int)pp->rho_a, (int)pp->rho_b, &pp->k);
 }
 
@@ -189,7 +194,6 @@ void describe_pass(efft_plan_s* pl, int p, int np, int64_t R, int64_t Ns) {
     d.cg = D * F;
     d.cs = F;
     d.ig = D * F;
-    d.if_ = 1;
     d.is = F;
     d.im = C;
     if (Ns == 1) {  // out[j*R + r]: transposed, unit stride along r
@@ -224,26 +228,28 @@ void describe_pass(efft_plan_s* pl, int p, int np, int64_t R, int64_t Ns) {
   const int64_t DB = pp.k.d_b;
   SubDesc& A = a.a;
   SubDesc& B = a.b;
-  // A: rows r = u + t*rb (task = u), rho_a-point DFT over t, into staging
+  // A: rows r = u + t*rb, u = task*DA + s, rho_a-point DFT over t, into staging
+  const int64_t DA = pp.k.d_a;
   A.ncols = C;
   A.cg = F;
   A.ig = F;
-  A.it = C;
-  A.if_ = 1;
+  A.it = DA * C;
+  A.is = C;
   A.im = rb * C;
   if (Ns != 1) {
     A.tw_mod = N;  // W_N^(j*r), j = grp*F + f, r = u + t*rb
     A.Ag = F;
     A.Af = 1;
-    A.Ct = 1;
+    A.Ct = DA;
+    A.Cs = 1;
     A.Cm = rb;
   }
   A.out_staging = 1;
-  A.ot = ra * F;  // staging (u*ra + k1)*F + f
-  A.of = 1;
+  A.ot = DA * ra * F;  // staging (u*ra + k1)*F + f
+  A.os = ra * F;
   A.om = F;
   A.store_mode = 0;
-  A.ntasks = (int32_t)rb;
+  A.ntasks = (int32_t)(rb / DA);
   A.conj_in = first && inverse;
   A.check_finite = first && (pl->flags & EFFT_FLAG_CHECK_FINITE);
   // B: k1 = task*DB + s, rho_b-point DFT over u with W_R^(k1*u)
@@ -252,7 +258,6 @@ void describe_pass(efft_plan_s* pl, int p, int np, int64_t R, int64_t Ns) {
   B.in_staging = 1;
   B.it = DB * F;
   B.is = F;
-  B.if_ = 1;
   B.im = ra * F;
   B.tw_mod = R;
   B.At = DB;
@@ -340,12 +345,17 @@ int build_plan(efft_plan_s* pl) {
     pp.grid = (int)grid;
     PassArgs& a = pp.args;
     if (pp.staged) {
+      // Tasks are grabbed in order; ~grid of them are in flight at once.  B(g)
+      // is issued `lag` steps after A(g) so its producers are done, and A(g)
+      // reuses the slot of group g - slots, issued slots - lag steps earlier,
+      // so slots - lag must also exceed the in-flight window.
       const int64_t per = a.a.ntasks + a.b.ntasks;
-      int64_t lag = (grid + per - 1) / per + 1;
-      lag = env_int("EFFT_LAG", (int)lag);
+      const int64_t inflight = grid * 3;  // a warp-specialised CTA holds up to 3 tasks
+      const int64_t window = (inflight + per - 1) / per;
+      int64_t lag = env_int("EFFT_LAG", (int)(window + 1));
       if (lag < 1) lag = 1;
       if (lag > a.ngroups) lag = a.ngroups;
-      int64_t slots = env_int("EFFT_SLOTS", (int)(lag + 2));
+      int64_t slots = env_int("EFFT_SLOTS", (int)(lag + window + 2));
       if (slots < lag + 1) slots = lag + 1;
       if (slots > a.ngroups) slots = a.ngroups;
       a.lag = (int32_t)lag;
@@ -486,6 +496,7 @@ int efft_execute(efft_plan_t pl, const void* d_in, void* d_out, void* stream) {
   CUDA_TRY(cudaSetDevice(pl->device));
   CUDA_TRY(cudaMemsetAsync(pl->counters, 0, pl->counter_bytes, s));
   for (int p = 0; p < pl->npass; ++p) {
+    if (pl->timing) CUDA_TRY(cudaEventRecord(pl->ev[p], s));
     PassArgs a = pl->pass[p].args;
     a.in = p == 0 ? d_in : d_out;
     a.out = d_out;
@@ -493,10 +504,12 @@ int efft_execute(efft_plan_t pl, const void* d_in, void* d_out, void* stream) {
     pp.k.fn<<<pp.grid, pp.k.nt, pp.k.smem_bytes, s>>>(a);
     CUDA_TRY(cudaGetLastError());
   }
+  if (pl->timing) CUDA_TRY(cudaEventRecord(pl->ev[pl->npass], s));
   if (pl->real_input) {
     const int64_t h = pl->n, work = h / 2 + 1;
     real_split_kernel<<<(unsigned)((work + 255) / 256), 256, 0, s>>>((float2*)d_out, h, pl->n_user);
     CUDA_TRY(cudaGetLastError());
+    if (pl->timing) CUDA_TRY(cudaEventRecord(pl->ev[pl->npass + 1], s));
   }
   return EFFT_OK;
 }
@@ -532,9 +545,30 @@ int efft_nonfinite_seen(efft_plan_t pl, int* seen, void* stream) {
   return EFFT_OK;
 }
 
+int efft_plan_enable_timing(efft_plan_t pl, int enable) {
+  if (!pl) return fail(EFFT_ERR_INVALID_ARG, "NULL plan");
+  CUDA_TRY(cudaSetDevice(pl->device));
+  if (enable && !pl->ev[0])
+    for (auto& e : pl->ev) CUDA_TRY(cudaEventCreate(&e));
+  pl->timing = enable != 0;
+  return EFFT_OK;
+}
+
+int efft_plan_launch_times(efft_plan_t pl, float* ms, int max_launches) {
+  if (!pl || !ms) return fail(EFFT_ERR_INVALID_ARG, "NULL argument");
+  if (!pl->timing) return fail(EFFT_ERR_INVALID_ARG, "timing not enabled");
+  const int nl = pl->npass + (pl->real_input ? 1 : 0);
+  CUDA_TRY(cudaSetDevice(pl->device));
+  for (int i = 0; i < nl && i < max_launches; ++i)
+    CUDA_TRY(cudaEventElapsedTime(&ms[i], pl->ev[i], pl->ev[i + 1]));
+  return EFFT_OK;
+}
+
 int efft_plan_destroy(efft_plan_t pl) {
   if (!pl) return EFFT_OK;
   cudaSetDevice(pl->device);
+  for (auto& e : pl->ev)
+    if (e) cudaEventDestroy(e);
   if (pl->staging) cudaFree(pl->staging);
   if (pl->counters) cudaFree(pl->counters);
   if (pl->flag) cudaFree(pl->flag);

@@ -18,30 +18,52 @@
 // each pass still costs one HBM read and one HBM write.
 //
 // A task ("tile") is F x D x RHO complex elements: F adjacent columns (F *
-// sizeof(complex) = 128 B, so every global access is a full 128-byte line and
-// every shared-memory row touches all 32 banks exactly once), D independent
-// DFTs, RHO points each.  The tile lives in registers (E elements per thread)
-// and is exchanged through padded shared memory between in-CTA radix stages.
+// sizeof(complex) = 128 B: every global access is a full 128-byte line read as
+// eight 16-byte vectors), D independent DFTs, RHO points each.  The tile lives
+// in registers (E elements per thread) and is exchanged through shared memory
+// rows padded to 144 B (16-byte aligned, conflict-free for row-, column- and
+// transposed accesses) between the in-CTA radix stages.
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
+
+#include <type_traits>
 
 #include "w192_table.cuh"
 
 namespace efft {
 
 // ----------------------------------------------------------------------------
+// compile-time loop
+// ----------------------------------------------------------------------------
+template <int I, int E, class Fn>
+__device__ __forceinline__ void cfor(Fn&& f) {
+  if constexpr (I < E) {
+    f(std::integral_constant<int, I>{});
+    cfor<I + 1, E>(f);
+  }
+}
+
+// ----------------------------------------------------------------------------
 // complex helpers
 // ----------------------------------------------------------------------------
 template <typename R> struct CT;
 template <> struct CT<float> {
-  using V = float2;
-  static constexpr int F = 16;
+  using V = float2;                 // one complex element
+  static constexpr int F = 16;      // columns per 128-byte row
+  static constexpr int VEC = 2;     // default elements per lane access (16 bytes)
 };
 template <> struct CT<double> {
   using V = double2;
   static constexpr int F = 8;
+  static constexpr int VEC = 1;
 };
+
+// access vector of VEC adjacent complex elements (one lane's global/smem access)
+template <typename R, int VEC> struct VecT;
+template <> struct VecT<float, 2> { using T = float4; };
+template <> struct VecT<float, 1> { using T = float2; };
+template <> struct VecT<double, 1> { using T = double2; };
 
 __device__ __forceinline__ float2 mk(float a, float b) { return make_float2(a, b); }
 __device__ __forceinline__ double2 mk(double a, double b) { return make_double2(a, b); }
@@ -53,32 +75,148 @@ template <typename V> __device__ __forceinline__ V cmul(V a, V b) {
 __device__ __forceinline__ float2 to_v(double2 w, float) { return make_float2((float)w.x, (float)w.y); }
 __device__ __forceinline__ double2 to_v(double2 w, double) { return w; }
 
-template <typename R> __device__ __forceinline__ typename CT<R>::V w192(int q);
-template <> __device__ __forceinline__ float2 w192<float>(int q) {
-  return make_float2(c_w192_float[q][0], c_w192_float[q][1]);
+// 16-byte vector <-> VEC complex elements
+__device__ __forceinline__ void unpack(float4 a, float2* v0, float2* v1) {
+  *v0 = make_float2(a.x, a.y);
+  *v1 = make_float2(a.z, a.w);
 }
-template <> __device__ __forceinline__ double2 w192<double>(int q) {
-  return make_double2(c_w192_double[q][0], c_w192_double[q][1]);
+__device__ __forceinline__ float4 pack(float2 a, float2 b) { return make_float4(a.x, a.y, b.x, b.y); }
+
+// ----------------------------------------------------------------------------
+// 16-byte global accesses with L2 eviction-priority hints.  The array being
+// transformed streams through L2 once per pass (evict_first); the staging ring
+// must stay resident between its producer and consumer tiles (evict_last), and
+// is discarded (no write-back) once consumed.
+// ----------------------------------------------------------------------------
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t policy_evict_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+template <typename VT>
+__device__ __forceinline__ VT ld_stream(const VT* ptr, uint64_t pol) {
+  if constexpr (sizeof(VT) == 16) {
+    uint4 r;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+                 : "l"(ptr), "l"(pol));
+    return *reinterpret_cast<VT*>(&r);
+  } else {
+    static_assert(sizeof(VT) == 8, "8- or 16-byte accesses");
+    uint2 r;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.u32 {%0,%1}, [%2], %3;"
+                 : "=r"(r.x), "=r"(r.y)
+                 : "l"(ptr), "l"(pol));
+    return *reinterpret_cast<VT*>(&r);
+  }
+}
+template <typename VT>
+__device__ __forceinline__ VT ld_staging(const VT* ptr) {
+  if constexpr (sizeof(VT) == 16) {
+    uint4 r;
+    asm volatile("ld.global.cg.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+                 : "l"(ptr));
+    return *reinterpret_cast<VT*>(&r);
+  } else {
+    uint2 r;
+    asm volatile("ld.global.cg.v2.u32 {%0,%1}, [%2];" : "=r"(r.x), "=r"(r.y) : "l"(ptr));
+    return *reinterpret_cast<VT*>(&r);
+  }
+}
+template <typename VT>
+__device__ __forceinline__ void st_hint(VT* ptr, VT v, uint64_t pol) {
+  if constexpr (sizeof(VT) == 16) {
+    const uint4 u = *reinterpret_cast<const uint4*>(&v);
+    asm volatile("st.global.cg.L2::cache_hint.v4.u32 [%0], {%1,%2,%3,%4}, %5;" ::"l"(ptr), "r"(u.x), "r"(u.y),
+                 "r"(u.z), "r"(u.w), "l"(pol)
+                 : "memory");
+  } else {
+    static_assert(sizeof(VT) == 8, "8- or 16-byte accesses");
+    const uint2 u = *reinterpret_cast<const uint2*>(&v);
+    asm volatile("st.global.cg.L2::cache_hint.v2.u32 [%0], {%1,%2}, %3;" ::"l"(ptr), "r"(u.x), "r"(u.y), "l"(pol)
+                 : "memory");
+  }
+}
+// Drop a consumed 128-byte staging line from L2 without writing it back.
+__device__ __forceinline__ void l2_discard(const void* ptr) {
+  asm volatile("discard.global.L2 [%0], 128;" ::"l"(ptr) : "memory");
 }
 
-// b * W_N^k with N | 192; k, N are compile-time after unrolling so the branches
-// fold and the table read becomes a constant-bank operand.
-template <typename R, int N>
-__device__ __forceinline__ typename CT<R>::V twk(typename CT<R>::V b, int k) {
+// ----------------------------------------------------------------------------
+// mbarrier + bulk asynchronous copy (TMA engine, cp.async.bulk) primitives
+// ----------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* ptr) {
+  return (uint32_t)__cvta_generic_to_shared(ptr);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      " .reg .pred p;\n"
+      "WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra WAIT_%=;\n"
+      "}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+// global -> shared bulk copy completing `bytes` transactions on `bar`
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
+                                         uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::
+          "r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+      : "memory");
+}
+// order generic-proxy writes observed through an acquire before async-proxy reads
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
+
+// b * W_N^K, N | 192, K compile-time: trivial roots become sign swaps, the
+// rest immediate-operand complex multiplies.
+template <typename R, int N, int K>
+__device__ __forceinline__ typename CT<R>::V twk(typename CT<R>::V b) {
   static_assert(192 % N == 0, "register DFT size must divide 192");
-  const int q = (k % N) * (192 / N);
-  if (q == 0) return b;
-  if (q == 48) return mk(b.y, -b.x);    // -i
-  if (q == 96) return mk(-b.x, -b.y);   // -1
-  if (q == 144) return mk(-b.y, b.x);   // +i
-  if (q == 24 || q == 72 || q == 120 || q == 168) {
-    typename CT<R>::V w = w192<R>(q);  // (+-1 +- i)/sqrt2
-    const R h = w.x > 0 ? w.x : -w.x;
-    const R sx = w.x > 0 ? R(1) : R(-1), sy = w.y > 0 ? R(1) : R(-1);
-    // (bx + i by)(sx + i sy) h
-    return mk((sx * b.x - sy * b.y) * h, (sx * b.y + sy * b.x) * h);
+  constexpr int Q = (K % N) * (192 / N);
+  if constexpr (Q == 0) {
+    return b;
+  } else if constexpr (Q == 48) {
+    return mk(b.y, -b.x);  // -i
+  } else if constexpr (Q == 96) {
+    return mk(-b.x, -b.y);
+  } else if constexpr (Q == 144) {
+    return mk(-b.y, b.x);  // +i
+  } else if constexpr (Q == 24) {  // (1 - i)/sqrt2
+    constexpr R h = (R)0.70710678118654752440084436210484903928;
+    return mk((b.x + b.y) * h, (b.y - b.x) * h);
+  } else if constexpr (Q == 72) {  // (-1 - i)/sqrt2
+    constexpr R h = (R)0.70710678118654752440084436210484903928;
+    return mk((b.y - b.x) * h, -(b.x + b.y) * h);
+  } else if constexpr (Q == 120) {  // (-1 + i)/sqrt2
+    constexpr R h = (R)0.70710678118654752440084436210484903928;
+    return mk(-(b.x + b.y) * h, (b.x - b.y) * h);
+  } else if constexpr (Q == 168) {  // (1 + i)/sqrt2
+    constexpr R h = (R)0.70710678118654752440084436210484903928;
+    return mk((b.x - b.y) * h, (b.x + b.y) * h);
+  } else {
+    constexpr R wr = (R)W192::v[Q][0], wi = (R)W192::v[Q][1];
+    return mk(fma(b.x, wr, -b.y * wi), fma(b.x, wi, b.y * wr));
   }
-  return cmul(b, w192<R>(q));
 }
 
 // ----------------------------------------------------------------------------
@@ -100,7 +238,7 @@ template <typename V> __device__ __forceinline__ void dft4(V* a) {
 }
 template <typename V> __device__ __forceinline__ void dft3(V* a) {
   using R = decltype(a[0].x);
-  const R c = R(0.86602540378443864676372317075293618);  // sin(2pi/3)
+  constexpr R c = R(0.86602540378443864676372317075293618);  // sin(2pi/3)
   V t1 = cadd(a[1], a[2]);
   V d = csub(a[1], a[2]);
   V t2 = mk(a[0].x - R(0.5) * t1.x, a[0].y - R(0.5) * t1.y);
@@ -110,59 +248,66 @@ template <typename V> __device__ __forceinline__ void dft3(V* a) {
   a[2] = csub(t2, t3);
 }
 
-template <int N> struct RegPlan {
-  static constexpr int has3 = (N % 3 == 0) ? 1 : 0;
-  static constexpr int P = has3 ? N / 3 : N;
-  static constexpr int lg = (P >= 64) ? 6 : (P >= 32) ? 5 : (P >= 16) ? 4 : (P >= 8) ? 3 : (P >= 4) ? 2 : (P >= 2) ? 1 : 0;
-  static constexpr int n4 = lg / 2, n2 = lg % 2;
-  static constexpr int NST = has3 + n4 + n2;
-  static constexpr int radix(int i) { return (has3 && i == 0) ? 3 : (i < has3 + n4) ? 4 : 2; }
-};
+// In-place decimation-in-frequency network over a contiguous segment
+// [B, B+L) of v: radix r = 3 (if 3 | L), else 4, else 2; twiddles
+// W_L^(j*k) are compile-time constants.  Output X[k] ends at v[dif_pos<N>(k)]
+// (mixed-radix digit reversal; free renaming, no register copies).
+constexpr int dif_radix_rt(int L) { return (L % 3 == 0) ? 3 : (L % 4 == 0) ? 4 : 2; }
+constexpr int dif_pos(int L, int k) {
+  // position of output k of an L-point in-place DIF transform
+  int pos = 0;
+  while (L > 1) {
+    const int r = dif_radix_rt(L);
+    const int q = L / r;
+    pos += (k % r) * q;
+    k /= r;
+    L = q;
+  }
+  return pos;
+}
 
-template <typename R, int N, int I, int NS>
-__device__ __forceinline__ void reg_stage(typename CT<R>::V* v) {
+template <typename R, int L, int B>
+__device__ __forceinline__ void dif_segment(typename CT<R>::V* v) {
   using V = typename CT<R>::V;
-  if constexpr (I < RegPlan<N>::NST) {
-    constexpr int r = RegPlan<N>::radix(I);
-    V o[N];
-#pragma unroll
-    for (int j = 0; j < N / r; ++j) {
-      const int k = j % NS;
+  if constexpr (L > 1) {
+    constexpr int r = dif_radix_rt(L);
+    constexpr int q = L / r;
+    cfor<0, q>([&](auto J) {
+      constexpr int j = decltype(J)::value;
       V a[r];
-#pragma unroll
-      for (int t = 0; t < r; ++t) a[t] = twk<R, NS * r>(v[j + t * (N / r)], k * t);
+      cfor<0, r>([&](auto T) { a[decltype(T)::value] = v[B + j + decltype(T)::value * q]; });
       if constexpr (r == 2) dft2(a);
       if constexpr (r == 3) dft3(a);
       if constexpr (r == 4) dft4(a);
-#pragma unroll
-      for (int t = 0; t < r; ++t) o[(j - k) * r + k + t * NS] = a[t];
-    }
-#pragma unroll
-    for (int j = 0; j < N; ++j) v[j] = o[j];
-    reg_stage<R, N, I + 1, NS * r>(v);
+      cfor<0, r>([&](auto T) {
+        constexpr int k = decltype(T)::value;
+        v[B + j + k * q] = twk<R, L, j * k>(a[k]);
+      });
+    });
+    cfor<0, r>([&](auto T) { dif_segment<R, q, B + decltype(T)::value * q>(v); });
   }
 }
 
 template <typename R, int N>
 __device__ __forceinline__ void reg_dft(typename CT<R>::V* v) {
-  if constexpr (N > 1) reg_stage<R, N, 0, 1>(v);
+  dif_segment<R, N, 0>(v);
 }
 
 // ----------------------------------------------------------------------------
-// pass descriptors (host-built, passed by value)
+// pass descriptors (host-built, passed by value as a __grid_constant__)
 // ----------------------------------------------------------------------------
 struct SubDesc {
-  int64_t ncols, cg, cs;        // column validity: grp*cg + s*cs + f < ncols
-  int64_t ig, it, if_, is, im;  // load offsets (elements)
-  int64_t og, ot, of, os, om;   // store offsets (elements)
-  int64_t tw_mod;               // modulus of the fused DIT twiddle, 0 = none
-  int64_t Ag, At, Af, As;       // A = grp*Ag + task*At + f*Af + s*As
-  int64_t C0, Ct, Cs, Cm;       // C = C0 + task*Ct + s*Cs + m*Cm ; e = A*C mod tw_mod
-  int32_t ntasks;               // tasks per column group
+  int64_t ncols, cg, cs;   // column validity: grp*cg + s*cs + f < ncols
+  int64_t ig, it, is, im;  // load offsets (elements); columns are unit stride
+  int64_t og, ot, of, os, om;  // store offsets (elements)
+  int64_t tw_mod;          // modulus of the fused DIT twiddle, 0 = none
+  int64_t Ag, At, Af, As;  // A = grp*Ag + task*At + f*Af + s*As
+  int64_t C0, Ct, Cs, Cm;  // C = C0 + task*Ct + s*Cs + m*Cm ; e = A*C mod tw_mod
+  int32_t ntasks;          // tasks per column group
   int32_t in_staging, out_staging;
-  int32_t store_mode;           // 0 direct (f fastest), 1 s fastest, 2 m fastest (via smem)
+  int32_t store_mode;      // 0 direct (f unit stride), 1 s unit stride, 2 m unit stride
   int32_t conj_in, conj_out, check_finite, pad_;
-  double scale;                 // output scale (1 = none)
+  double scale;            // output scale (applied with conj_out)
 };
 
 struct PassArgs {
@@ -200,7 +345,7 @@ __device__ __forceinline__ double2 wroot(int64_t e, int64_t M) {
 }
 
 // ----------------------------------------------------------------------------
-// in-CTA stage plan: radices sigma_i | E, prod sigma_i = RHO
+// in-CTA stage plan: radices sigma_i | EV, prod sigma_i = RHO
 // ----------------------------------------------------------------------------
 struct StagePlan {
   int n;
@@ -225,20 +370,40 @@ constexpr StagePlan make_stage_plan(int rho, int e) {
   return p;
 }
 
-template <typename R, int RHO_, int D_, int NT_>
+template <typename R, int RHO_, int D_, int NT_, bool MASK_, int VEC_, int TOFF_ = 0, int BAR_ = 0>
 struct Tile {
+  static constexpr int TOFF = TOFF_, BAR = BAR_;
+  // tile-thread index and the barrier over the tile's threads (named barrier
+  // when the tile threads are the consumer warps of a warp-specialised CTA)
+  __device__ __forceinline__ static int tx() { return (int)threadIdx.x - TOFF; }
+  __device__ __forceinline__ static void tsync() {
+    if constexpr (BAR == 0)
+      tsync();
+    else
+      asm volatile("bar.sync %0, %1;" ::"n"(BAR), "n"(NT_) : "memory");
+  }
   using V = typename CT<R>::V;
+  static constexpr int VEC = VEC_;
+  using VT = typename VecT<R, VEC>::T;
   static constexpr int RHO = RHO_, D = D_, NT = NT_;
+  static constexpr bool MASK = MASK_;
   static constexpr int F = CT<R>::F;
+  static constexpr int FV = F / VEC;     // lanes per 128-byte row (8)
+  static constexpr int PADF = F + 16 / (int)sizeof(V);  // smem row: 144 bytes, 16-byte aligned
   static constexpr int TILE = F * D * RHO;
-  static constexpr int E = TILE / NT;
-  static_assert(E * NT == TILE, "tile must split evenly over threads");
-  static constexpr StagePlan PL = make_stage_plan(RHO, E);
+  static constexpr int E = TILE / NT;    // complex elements per thread
+  static constexpr int EV = E / VEC;     // butterfly elements per column-lane
+  static_assert(E * NT == TILE && EV * VEC == E, "tile must split evenly over threads");
+  static_assert(NT % FV == 0, "threads must cover whole rows");
+  static constexpr StagePlan PL = make_stage_plan(RHO, EV);
   static_assert(PL.n > 0, "no stage plan for this tile");
   static constexpr int NST = PL.n;
-  static constexpr int SMEM_ELEMS = D * RHO * (F + 1);
+  static constexpr int SMEM_ELEMS = D * RHO * PADF;
 
-  __device__ __forceinline__ static int sidx(int f, int s, int m) { return (m * D + s) * (F + 1) + f; }
+  __device__ __forceinline__ static int sidx(int f, int s, int m) { return (m * D + s) * PADF + f; }
+
+  // register position of output t of an S-point in-place DFT
+  static constexpr int P(int S, int t) { return dif_pos(S, t); }
 
   static constexpr int prod_before(int i) {
     int p = 1;
@@ -246,58 +411,88 @@ struct Tile {
     return p;
   }
 
-  // per-CTA table W_RHO^i, i < RHO, fp64 sincospi then rounded once
+  // per-CTA table W_RHO^i, i < RHO, fp64 sincospi rounded once
   __device__ static void build_table(V* tw) {
-    for (int i = threadIdx.x; i < RHO; i += blockDim.x) tw[i] = to_v(wroot(i, RHO), R());
+    for (int i = threadIdx.x; i < RHO; i += blockDim.x) tw[i] = to_v(wroot(i, RHO), R());  // all CTA threads
+  }
+
+  // thread-butterfly q of a stage with radix S: (column lane, u, s)
+  template <int S>
+  __device__ __forceinline__ static void coords(int q, int& fv, int& u, int& s) {
+    constexpr int L = RHO / S;
+    const int g = tx() + q * NT;
+    fv = g % FV;
+    const int x = g / FV;
+    u = x % L;
+    s = x / L;
+  }
+
+  __device__ __forceinline__ static void put(V* sm, int f, int s, int m, const V* v0, const V* v1) {
+    if constexpr (VEC == 2)
+      *reinterpret_cast<VT*>(sm + sidx(f, s, m)) = pack(*v0, *v1);
+    else
+      sm[sidx(f, s, m)] = *v0;
+  }
+  __device__ __forceinline__ static void get(const V* sm, int f, int s, int m, V* v0, V* v1) {
+    if constexpr (VEC == 2)
+      unpack(*reinterpret_cast<const VT*>(sm + sidx(f, s, m)), v0, v1);
+    else
+      *v0 = sm[sidx(f, s, m)];
   }
 
   template <int I>
   __device__ __forceinline__ static void stage_compute(V* v, const V* tw) {
     constexpr int S = PL.sig[I];
-    constexpr int Q = E / S;
-    constexpr int L = RHO / S;
+    constexpr int Q = EV / S;
     constexpr int NS = prod_before(I);
 #pragma unroll
     for (int q = 0; q < Q; ++q) {
-      if constexpr (I > 0 && NS > 1) {
-        const int g = threadIdx.x + q * NT;
-        const int u = (g / F) % L;
+      if constexpr (I > 0) {
+        int fv, u, s;
+        coords<S>(q, fv, u, s);
         const int k = u % NS;
         constexpr int STEP = RHO / (NS * S);
 #pragma unroll
-        for (int t = 1; t < S; ++t) v[q * S + t] = cmul(v[q * S + t], tw[k * t * STEP]);
+        for (int t = 1; t < S; ++t) {
+          const V w = tw[k * t * STEP];
+#pragma unroll
+          for (int c = 0; c < VEC; ++c) v[(q * VEC + c) * S + t] = cmul(v[(q * VEC + c) * S + t], w);
+        }
       }
-      reg_dft<R, S>(v + q * S);
+#pragma unroll
+      for (int c = 0; c < VEC; ++c) reg_dft<R, S>(v + (q * VEC + c) * S);
     }
   }
 
   template <int I>
-  __device__ __forceinline__ static void stage_write(V* v, V* sm) {
+  __device__ __forceinline__ static void stage_write(const V* v, V* sm) {
     constexpr int S = PL.sig[I];
-    constexpr int Q = E / S;
-    constexpr int L = RHO / S;
+    constexpr int Q = EV / S;
     constexpr int NS = prod_before(I);
 #pragma unroll
     for (int q = 0; q < Q; ++q) {
-      const int g = threadIdx.x + q * NT;
-      const int f = g % F, x = g / F, u = x % L, s = x / L;
+      int fv, u, s;
+      coords<S>(q, fv, u, s);
       const int k = u % NS;
 #pragma unroll
-      for (int t = 0; t < S; ++t) sm[sidx(f, s, (u - k) * S + k + t * NS)] = v[q * S + t];
+      for (int t = 0; t < S; ++t)
+        put(sm, fv * VEC, s, (u - k) * S + k + t * NS, &v[(q * VEC) * S + P(S, t)],
+            &v[(q * VEC + VEC - 1) * S + P(S, t)]);
     }
   }
 
   template <int I>
   __device__ __forceinline__ static void stage_read(V* v, const V* sm) {
     constexpr int S = PL.sig[I];
-    constexpr int Q = E / S;
+    constexpr int Q = EV / S;
     constexpr int L = RHO / S;
 #pragma unroll
     for (int q = 0; q < Q; ++q) {
-      const int g = threadIdx.x + q * NT;
-      const int f = g % F, x = g / F, u = x % L, s = x / L;
+      int fv, u, s;
+      coords<S>(q, fv, u, s);
 #pragma unroll
-      for (int t = 0; t < S; ++t) v[q * S + t] = sm[sidx(f, s, u + t * L)];
+      for (int t = 0; t < S; ++t)
+        get(sm, fv * VEC, s, u + t * L, &v[(q * VEC) * S + t], &v[(q * VEC + VEC - 1) * S + t]);
     }
   }
 
@@ -306,116 +501,308 @@ struct Tile {
     if constexpr (I < NST) {
       if constexpr (I > 0) {
         stage_read<I>(v, sm);
-        __syncthreads();
+        tsync();
       }
       stage_compute<I>(v, tw);
       if constexpr (I + 1 < NST) {
         stage_write<I>(v, sm);
-        __syncthreads();
+        tsync();
       }
       stages<I + 1>(v, sm, tw);
     }
   }
 
-  // One tile: load (+conj, +finite check, +DIT twiddle), RHO-point DFTs, store.
-  __device__ static void run(const SubDesc& d, const PassArgs& p, int64_t grp, int task, V* sm,
-                             const V* tw, bool& nonfinite) {
-    V v[E];
+  // ---- stage-0 load: 16-byte vectors, columns unit stride
+  template <bool CONJ, bool CHECK>
+  __device__ __forceinline__ static void load(const SubDesc& d, const V* src, int64_t grp, V* v,
+                                              bool& nonfinite) {
     constexpr int S0 = PL.sig[0];
-    constexpr int Q0 = E / S0;
+    constexpr int Q0 = EV / S0;
     constexpr int L0 = RHO / S0;
-    const V* src = d.in_staging
-                       ? (const V*)p.staging + (grp % p.nslots) * p.slot_elems + task * d.it
-                       : (const V*)p.in + grp * d.ig + task * d.it;
-    // ---- load in the stage-0 arrangement (f fastest: 128-byte runs)
+    const bool stg = d.in_staging;
+    const uint64_t pol = policy_evict_first();
 #pragma unroll
     for (int q = 0; q < Q0; ++q) {
-      const int g = threadIdx.x + q * NT;
-      const int f = g % F, x = g / F, u = x % L0, s = x / L0;
-      const bool valid = grp * d.cg + s * d.cs + f < d.ncols;
-      const V* bp = src + f * d.if_ + s * d.is + u * d.im;
+      int fv, u, s;
+      coords<S0>(q, fv, u, s);
+      const int f0 = fv * VEC;
+      const V* bp = src + f0 + s * d.is + u * d.im;
+      const int64_t step = (int64_t)L0 * d.im;
+      bool valid[VEC];
+#pragma unroll
+      for (int c = 0; c < VEC; ++c) valid[c] = !MASK || grp * d.cg + s * d.cs + f0 + c < d.ncols;
 #pragma unroll
       for (int t = 0; t < S0; ++t) {
-        V x0 = mk(R(0), R(0));
-        if (valid) x0 = d.in_staging ? __ldcg(bp + (int64_t)t * L0 * d.im) : __ldg(bp + (int64_t)t * L0 * d.im);
-        if (d.conj_in) x0.y = -x0.y;
-        if (d.check_finite && !(isfinite(x0.x) && isfinite(x0.y))) nonfinite = true;
-        v[q * S0 + t] = x0;
+        V x[VEC];
+        if constexpr (MASK) {
+#pragma unroll
+          for (int c = 0; c < VEC; ++c) x[c] = valid[c] ? bp[c] : mk(R(0), R(0));
+        } else {
+          const VT* vp = reinterpret_cast<const VT*>(bp);
+          const VT a = stg ? ld_staging(vp) : ld_stream(vp, pol);
+          if constexpr (VEC == 2)
+            unpack(a, &x[0], &x[1]);
+          else
+            x[0] = *reinterpret_cast<const V*>(&a);
+        }
+#pragma unroll
+        for (int c = 0; c < VEC; ++c) {
+          if constexpr (CONJ) x[c].y = -x[c].y;
+          if constexpr (CHECK) nonfinite |= !(isfinite(x[c].x) && isfinite(x[c].y));
+          v[(q * VEC + c) * S0 + t] = x[c];
+        }
+        bp += step;
       }
-      if (d.tw_mod) {
-        const int64_t M = d.tw_mod;
-        const int64_t A = grp * d.Ag + task * d.At + f * d.Af + s * d.As;
-        const int64_t C = d.C0 + task * d.Ct + s * d.Cs + (int64_t)u * d.Cm;
+    }
+  }
+
+  // Every 128-byte staging row this tile read is discarded by the first lane
+  // of its row (each row is consumed by exactly one tile).
+  __device__ __forceinline__ static void discard_loaded(const SubDesc& d, const V* src) {
+    constexpr int S0 = PL.sig[0];
+    constexpr int Q0 = EV / S0;
+    constexpr int L0 = RHO / S0;
+#pragma unroll
+    for (int q = 0; q < Q0; ++q) {
+      int fv, u, s;
+      coords<S0>(q, fv, u, s);
+      if (fv != 0) continue;
+      const V* bp = src + s * d.is + u * d.im;
+      const int64_t step = (int64_t)L0 * d.im;
+#pragma unroll
+      for (int t = 0; t < S0; ++t) {
+        l2_discard(bp);
+        bp += step;
+      }
+    }
+  }
+
+  __device__ __forceinline__ static void twiddle(const SubDesc& d, int64_t grp, int task, V* v) {
+    constexpr int S0 = PL.sig[0];
+    constexpr int Q0 = EV / S0;
+    constexpr int L0 = RHO / S0;
+    const int64_t M = d.tw_mod;
+#pragma unroll
+    for (int q = 0; q < Q0; ++q) {
+      int fv, u, s;
+      coords<S0>(q, fv, u, s);
+      const int64_t C = d.C0 + task * d.Ct + s * d.Cs + (int64_t)u * d.Cm;
+      if (VEC > 1 && d.Af == 0) {  // one twiddle series serves all VEC columns
+        const int64_t A = grp * d.Ag + task * d.At + s * d.As;
         double2 w = wroot(mulmod(A, C, M), M);
         const double2 st = wroot(mulmod(A, d.Cm * L0, M), M);
 #pragma unroll
         for (int t = 0; t < S0; ++t) {
-          v[q * S0 + t] = cmul(v[q * S0 + t], to_v(w, R()));
+          const V wv = to_v(w, R());
+#pragma unroll
+          for (int c = 0; c < VEC; ++c) v[(q * VEC + c) * S0 + t] = cmul(v[(q * VEC + c) * S0 + t], wv);
+          if (t + 1 < S0) w = cmul(w, st);
+        }
+        continue;
+      }
+#pragma unroll
+      for (int c = 0; c < VEC; ++c) {
+        const int64_t A = grp * d.Ag + task * d.At + (fv * VEC + c) * d.Af + s * d.As;
+        double2 w = wroot(mulmod(A, C, M), M);
+        const double2 st = wroot(mulmod(A, d.Cm * L0, M), M);
+        V* vv = v + (q * VEC + c) * S0;
+#pragma unroll
+        for (int t = 0; t < S0; ++t) {
+          vv[t] = cmul(vv[t], to_v(w, R()));
           if (t + 1 < S0) w = cmul(w, st);
         }
       }
     }
-    // ---- in-CTA radix stages
-    stages<0>(v, sm, tw);
-    // ---- store (last stage holds m' = u + t*L for its butterflies)
+  }
+
+  // ---- store, direct (f unit stride) from the last stage's registers
+  template <bool CS>
+  __device__ __forceinline__ static void store_direct(const SubDesc& d, V* dst, int64_t grp, const V* v) {
     constexpr int SL = PL.sig[NST - 1];
-    constexpr int QL = E / SL;
+    constexpr int QL = EV / SL;
     constexpr int LL = RHO / SL;
-    V* dst = d.out_staging ? (V*)p.staging + (grp % p.nslots) * p.slot_elems + task * d.ot
-                           : (V*)p.out + grp * d.og + task * d.ot;
     const R sc = (R)d.scale;
-    if (d.store_mode == 0) {
+    const bool stg = d.out_staging;
+    const uint64_t pol = stg ? policy_evict_last() : policy_evict_first();
 #pragma unroll
-      for (int q = 0; q < QL; ++q) {
-        const int g = threadIdx.x + q * NT;
-        const int f = g % F, x = g / F, u = x % LL, s = x / LL;
-        if (grp * d.cg + s * d.cs + f >= d.ncols) continue;
-        V* bp = dst + f * d.of + s * d.os + u * d.om;
+    for (int q = 0; q < QL; ++q) {
+      int fv, u, s;
+      coords<SL>(q, fv, u, s);
+      const int f0 = fv * VEC;
+      V* bp = dst + f0 + s * d.os + u * d.om;
+      const int64_t step = (int64_t)LL * d.om;
+      bool valid[VEC];
 #pragma unroll
-        for (int t = 0; t < SL; ++t) {
-          V y = v[q * SL + t];
-          if (d.conj_out) y.y = -y.y;
-          if (d.scale != 1.0) y = mk(y.x * sc, y.y * sc);
-          if (d.out_staging)
-            __stcg(bp + (int64_t)t * LL * d.om, y);
-          else
-            bp[(int64_t)t * LL * d.om] = y;
+      for (int c = 0; c < VEC; ++c) valid[c] = !MASK || grp * d.cg + s * d.cs + f0 + c < d.ncols;
+#pragma unroll
+      for (int t = 0; t < SL; ++t) {
+        V y[VEC];
+#pragma unroll
+        for (int c = 0; c < VEC; ++c) {
+          y[c] = v[(q * VEC + c) * SL + P(SL, t)];
+          if constexpr (CS) y[c] = mk(y[c].x * sc, -y[c].y * sc);
         }
-      }
-    } else {
-      // transpose through shared memory so the output's unit-stride index is fastest
+        if constexpr (MASK) {
 #pragma unroll
-      for (int q = 0; q < QL; ++q) {
-        const int g = threadIdx.x + q * NT;
-        const int f = g % F, x = g / F, u = x % LL, s = x / LL;
-#pragma unroll
-        for (int t = 0; t < SL; ++t) sm[sidx(f, s, u + t * LL)] = v[q * SL + t];
-      }
-      __syncthreads();
-#pragma unroll 4
-      for (int q = 0; q < E; ++q) {
-        const int o = threadIdx.x + q * NT;
-        int f, s, m;
-        if (d.store_mode == 1) {
-          s = o % D;
-          f = (o / D) % F;
-          m = o / (D * F);
+          for (int c = 0; c < VEC; ++c)
+            if (valid[c]) bp[c] = y[c];
+        } else if constexpr (VEC == 2) {
+          st_hint(reinterpret_cast<VT*>(bp), pack(y[0], y[1]), pol);
         } else {
-          m = o % RHO;
-          s = (o / RHO) % D;
-          f = o / (RHO * D);
+          st_hint(bp, y[0], pol);
         }
-        if (grp * d.cg + s * d.cs + f >= d.ncols) continue;
-        V y = sm[sidx(f, s, m)];
-        if (d.conj_out) y.y = -y.y;
-        if (d.scale != 1.0) y = mk(y.x * sc, y.y * sc);
-        V* ptr = dst + f * d.of + s * d.os + (int64_t)m * d.om;
-        if (d.out_staging)
-          __stcg(ptr, y);
-        else
-          *ptr = y;
+        bp += step;
       }
     }
+  }
+
+  // ---- store through shared memory so the output's unit-stride index is fastest
+  template <bool CS, int MODE>
+  __device__ __forceinline__ static void store_transposed(const SubDesc& d, V* dst, int64_t grp, const V* v,
+                                                          V* sm) {
+    constexpr int SL = PL.sig[NST - 1];
+    constexpr int QL = EV / SL;
+    constexpr int LL = RHO / SL;
+#pragma unroll
+    for (int q = 0; q < QL; ++q) {
+      int fv, u, s;
+      coords<SL>(q, fv, u, s);
+#pragma unroll
+      for (int t = 0; t < SL; ++t)
+        put(sm, fv * VEC, s, u + t * LL, &v[(q * VEC) * SL + P(SL, t)], &v[(q * VEC + VEC - 1) * SL + P(SL, t)]);
+    }
+    tsync();
+    constexpr int FAST = MODE == 1 ? D : RHO;
+    constexpr int W = (FAST % VEC == 0) ? VEC : 1;  // outputs per lane (one 16-byte store)
+    constexpr int NO = TILE / W;
+    const R sc = (R)d.scale;
+    const uint64_t pol = policy_evict_first();
+#pragma unroll 4
+    for (int o0 = tx(); o0 < NO; o0 += NT) {
+      const int o = o0 * W;
+      int f, s, m;
+      if constexpr (MODE == 1) {
+        s = o % D;
+        f = (o / D) % F;
+        m = o / (D * F);
+      } else {
+        m = o % RHO;
+        s = (o / RHO) % D;
+        f = o / (RHO * D);
+      }
+      if (MASK && grp * d.cg + s * d.cs + f >= d.ncols) continue;
+      V y[W];
+#pragma unroll
+      for (int w = 0; w < W; ++w) {
+        y[w] = MODE == 1 ? sm[sidx(f, s + w, m)] : sm[sidx(f, s, m + w)];
+        if constexpr (CS) y[w] = mk(y[w].x * sc, -y[w].y * sc);
+      }
+      V* ptr = dst + f * d.of + s * d.os + (int64_t)m * d.om;
+      if constexpr (W == 2)
+        st_hint(reinterpret_cast<float4*>(ptr), pack(y[0], y[W - 1]), pol);
+      else
+        st_hint(ptr, y[0], pol);
+    }
+  }
+
+  __device__ __forceinline__ static void store(const SubDesc& d, const PassArgs& p, int64_t grp, int task,
+                                               const V* v, V* sm) {
+    const int64_t slot = d.out_staging ? grp % p.nslots : 0;
+    V* dst = d.out_staging ? (V*)p.staging + slot * p.slot_elems + task * d.ot
+                           : (V*)p.out + grp * d.og + task * d.ot;
+    const bool cs = d.conj_out;
+    if (d.store_mode == 0) {
+      if (cs)
+        store_direct<true>(d, dst, grp, v);
+      else
+        store_direct<false>(d, dst, grp, v);
+    } else if (d.store_mode == 1) {
+      if (cs)
+        store_transposed<true, 1>(d, dst, grp, v, sm);
+      else
+        store_transposed<false, 1>(d, dst, grp, v, sm);
+    } else {
+      if (cs)
+        store_transposed<true, 2>(d, dst, grp, v, sm);
+      else
+        store_transposed<false, 2>(d, dst, grp, v, sm);
+    }
+  }
+
+  // One tile: load (+conj, +finite check, +DIT twiddle), RHO-point DFTs, store.
+  __device__ static void run(const SubDesc& d, const PassArgs& p, int64_t grp, int task, V* sm,
+                             const V* tw, bool& nonfinite, int32_t* release = nullptr) {
+    V v[E];
+    const int64_t slot = d.in_staging ? grp % p.nslots : 0;
+    const V* src = d.in_staging ? (const V*)p.staging + slot * p.slot_elems + task * d.it
+                                : (const V*)p.in + grp * d.ig + task * d.it;
+    if (d.conj_in) {
+      if (d.check_finite)
+        load<true, true>(d, src, grp, v, nonfinite);
+      else
+        load<true, false>(d, src, grp, v, nonfinite);
+    } else if (d.check_finite) {
+      load<false, true>(d, src, grp, v, nonfinite);
+    } else {
+      load<false, false>(d, src, grp, v, nonfinite);
+    }
+    if (d.tw_mod) twiddle(d, grp, task, v);
+    // in-CTA radix stages; stage 0 consumes the loaded registers, after which the
+    // staging slot this tile read can be released to its producers
+    if (release != nullptr) {
+      stage_compute<0>(v, tw);
+      discard_loaded(d, src);
+      tsync();
+      if (tx() == 0) {
+        __threadfence();
+        atomicAdd(release, 1);
+      }
+      if constexpr (NST > 1) {
+        stage_write<0>(v, sm);
+        tsync();
+        stages<1>(v, sm, tw);
+      }
+    } else {
+      stages<0>(v, sm, tw);
+    }
+    store(d, p, grp, task, v, sm);
+  }
+
+  __device__ __forceinline__ static void fixup(const SubDesc& d, V* v, bool& nonfinite) {
+    const bool cj = d.conj_in, ck = d.check_finite;
+#pragma unroll
+    for (int i = 0; i < E; ++i) {
+      if (cj) v[i].y = -v[i].y;
+      if (ck) nonfinite |= !(isfinite(v[i].x) && isfinite(v[i].y));
+    }
+  }
+
+  // Warp-specialised variant: the producer warp has copied the tile's 128-byte
+  // rows into `buf` (padded rows, mbarrier-signalled); `buf` then doubles as
+  // the exchange buffer.  If `release` is set the rows came from the L2
+  // staging ring at `stg`: they are discarded (no write-back) and the slot is
+  // released to the producers of the next group.
+  __device__ static void run_smem(const SubDesc& d, const PassArgs& p, int64_t grp, int task, V* buf,
+                                  const V* tw, bool& nonfinite, int32_t* release, const V* stg) {
+    V v[E];
+    if (release != nullptr) {
+      for (int r = tx(); r < D * RHO; r += NT) l2_discard(stg + (r % D) * d.is + (int64_t)(r / D) * d.im);
+    }
+    stage_read<0>(v, buf);
+    tsync();  // every tile thread has its stage-0 data (and issued its discards)
+    if (release != nullptr && tx() == 0) {
+      __threadfence();
+      atomicAdd(release, 1);
+    }
+    if (d.conj_in || d.check_finite) fixup(d, v, nonfinite);
+    if (d.tw_mod) twiddle(d, grp, task, v);
+    stage_compute<0>(v, tw);
+    if constexpr (NST > 1) {
+      stage_write<0>(v, buf);
+      tsync();
+      stages<1>(v, buf, tw);
+    }
+    store(d, p, grp, task, v, buf);
   }
 };
 
@@ -426,25 +813,17 @@ struct NoTile {
 
 __device__ __forceinline__ void wait_at_least(const int32_t* ctr, int32_t need) {
   if (threadIdx.x == 0) {
-    while (*(volatile const int32_t*)ctr < need) __nanosleep(128);
+    while (*(volatile const int32_t*)ctr < need) __nanosleep(64);
     __threadfence();
   }
   __syncthreads();
-}
-
-__device__ __forceinline__ void signal_done(int32_t* ctr) {
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    __threadfence();
-    atomicAdd(ctr, 1);
-  }
 }
 
 // Persistent pass kernel: CTAs pull tasks from one global counter in a fixed
 // order (A(0..lag-1), then B(g-lag), A(g) pairs, then the tail of B), which
 // makes every wait target a task that an already-running CTA owns.
 template <typename R, class TA, class TB>
-__global__ void __launch_bounds__(TA::NT) pass_kernel(const PassArgs p) {
+__global__ void __launch_bounds__(TA::NT, (TA::NT >= 512 ? 1 : 2)) pass_kernel(const __grid_constant__ PassArgs p) {
   using V = typename CT<R>::V;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   constexpr int SM_ELEMS = TA::SMEM_ELEMS > TB::SMEM_ELEMS ? TA::SMEM_ELEMS : TB::SMEM_ELEMS;
@@ -455,18 +834,20 @@ __global__ void __launch_bounds__(TA::NT) pass_kernel(const PassArgs p) {
   TA::build_table(twA);
   if constexpr (TB::RHO > 0) TB::build_table(twB);
   bool nonfinite = false;
+  if (threadIdx.x == 0) s_task = atomicAdd(p.task_counter, 1ull);
   for (;;) {
-    if (threadIdx.x == 0) s_task = atomicAdd(p.task_counter, 1ull);
     __syncthreads();
     const int64_t pos = (int64_t)s_task;
     if (pos >= p.total_tasks) break;
-    if (!p.staged) {
+    // claim the next task now; its latency hides behind this task's work
+    // (deadlock-free: the smallest unfinished task is always a running one)
+    unsigned long long next = 0;
+    if (threadIdx.x == 0) next = atomicAdd(p.task_counter, 1ull);
+    if constexpr (TB::RHO == 0) {
       const int64_t grp = pos / p.a.ntasks;
       TA::run(p.a, p, grp, (int)(pos % p.a.ntasks), sm, twA, nonfinite);
       __syncthreads();
-      continue;
-    }
-    if constexpr (TB::RHO > 0) {
+    } else {
       const int64_t G = p.ngroups, L = p.lag, TAn = p.a.ntasks, TBn = p.b.ntasks;
       bool isB;
       int64_t grp, sub;
@@ -495,15 +876,156 @@ __global__ void __launch_bounds__(TA::NT) pass_kernel(const PassArgs p) {
       if (!isB) {
         if (grp >= p.nslots) wait_at_least(p.doneB + (grp - p.nslots), (int32_t)TBn);
         TA::run(p.a, p, grp, (int)sub, sm, twA, nonfinite);
-        signal_done(p.doneA + grp);
+        __syncthreads();
+        if (threadIdx.x == 0) {
+          __threadfence();
+          atomicAdd(p.doneA + grp, 1);
+        }
       } else {
         wait_at_least(p.doneA + grp, (int32_t)TAn);
-        TB::run(p.b, p, grp, (int)sub, sm, twB, nonfinite);
-        signal_done(p.doneB + grp);
+        TB::run(p.b, p, grp, (int)sub, sm, twB, nonfinite, p.doneB + grp);
+        __syncthreads();
       }
     }
+    if (threadIdx.x == 0) s_task = next;
   }
   if (__syncthreads_or(nonfinite) && threadIdx.x == 0) atomicOr(p.flag, 1);
+}
+
+// Task order of a staged pass: A(0..lag-1), then pairs [B(g-lag), A(g)], then
+// the remaining B.  Every dependency (B(g) on A(g), A(g) on the slot released
+// by B(g-nslots)) points to an earlier task.
+__device__ __forceinline__ void decode_task(const PassArgs& p, int64_t pos, bool& isB, int64_t& grp,
+                                            int64_t& sub) {
+  const int64_t G = p.ngroups, L = p.lag, TAn = p.a.ntasks, TBn = p.b.ntasks;
+  if (pos < L * TAn) {
+    isB = false;
+    grp = pos / TAn;
+    sub = pos % TAn;
+  } else if (pos < L * TAn + (G - L) * (TAn + TBn)) {
+    const int64_t q = pos - L * TAn;
+    const int64_t i = L + q / (TAn + TBn), r = q % (TAn + TBn);
+    if (r < TBn) {
+      isB = true;
+      grp = i - L;
+      sub = r;
+    } else {
+      isB = false;
+      grp = i;
+      sub = r - TBn;
+    }
+  } else {
+    const int64_t q = pos - L * TAn - (G - L) * (TAn + TBn);
+    isB = true;
+    grp = G - L + q / TBn;
+    sub = q % TBn;
+  }
+}
+
+// Warp-specialised staged pass (one CTA per SM, persistent).
+//   warp 0 (producer): claims tasks in order, resolves their dependency, and
+//     copies the tile's 128-byte rows (HBM input for A tasks, the L2 staging
+//     ring for B tasks) into one of two shared-memory buffers with
+//     cp.async.bulk, completing an mbarrier -- the next tile streams in while
+//     the consumers work on the current one.
+//   warps 1.. (consumers): wait on the buffer's mbarrier, run the tile
+//     (registers + the same buffer for exchanges, named barrier 1), store,
+//     then release the buffer (empty mbarrier) and, for A tasks, publish the
+//     group counter.
+template <typename R, class TA, class TB>
+__global__ void __launch_bounds__(TA::NT + 32, 1) staged_kernel(const __grid_constant__ PassArgs p) {
+  using V = typename CT<R>::V;
+  static_assert(TA::NT == TB::NT && TA::TOFF == 32 && TB::TOFF == 32, "consumer warps follow warp 0");
+  static_assert(TA::PADF == TB::PADF, "same row pitch");
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  constexpr int BUF = TA::SMEM_ELEMS > TB::SMEM_ELEMS ? TA::SMEM_ELEMS : TB::SMEM_ELEMS;
+  V* bufs = reinterpret_cast<V*>(smem_raw);
+  V* twA = bufs + 2 * BUF;
+  V* twB = twA + TA::RHO;
+  __shared__ __align__(8) uint64_t full[2], empty[2];
+  __shared__ long long task_of[2];
+  if (threadIdx.x == 0) {
+    mbar_init(&full[0], 1);
+    mbar_init(&full[1], 1);
+    mbar_init(&empty[0], TA::NT / 32);
+    mbar_init(&empty[1], TA::NT / 32);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  TA::build_table(twA);
+  TB::build_table(twB);
+  __syncthreads();
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  if (warp == 0) {
+    const uint64_t pol = policy_evict_first();
+    for (int64_t k = 0;; ++k) {
+      const int b = (int)(k & 1);
+      if (k >= 2) mbar_wait(&empty[b], (uint32_t)(((k >> 1) - 1) & 1));
+      unsigned long long pos = 0;
+      if (lane == 0) pos = atomicAdd(p.task_counter, 1ull);
+      pos = __shfl_sync(0xffffffffu, pos, 0);
+      if ((int64_t)pos >= p.total_tasks) {
+        if (lane == 0) {
+          task_of[b] = -1;
+          mbar_arrive(&full[b]);
+        }
+        break;
+      }
+      bool isB;
+      int64_t grp, sub;
+      decode_task(p, (int64_t)pos, isB, grp, sub);
+      if (lane == 0) {
+        const int32_t* ctr = isB ? p.doneA + grp : (grp >= p.nslots ? p.doneB + (grp - p.nslots) : nullptr);
+        const int32_t need = isB ? p.a.ntasks : p.b.ntasks;
+        if (ctr != nullptr) {
+          while (*(volatile const int32_t*)ctr < need) __nanosleep(32);
+          __threadfence();
+        }
+        fence_proxy_async();
+        task_of[b] = (long long)pos;
+        const int rows = isB ? TB::D * TB::RHO : TA::D * TA::RHO;
+        mbar_arrive_tx(&full[b], (uint32_t)rows * 128u);
+      }
+      __syncwarp();
+      const SubDesc& d = isB ? p.b : p.a;
+      const int Dt = isB ? TB::D : TA::D;
+      const int rows = isB ? TB::D * TB::RHO : TA::D * TA::RHO;
+      const V* src = d.in_staging ? (const V*)p.staging + (grp % p.nslots) * p.slot_elems + sub * d.it
+                                  : (const V*)p.in + grp * d.ig + sub * d.it;
+      V* dst = bufs + b * BUF;
+      for (int r = lane; r < rows; r += 32) {
+        const int s = r % Dt, m = r / Dt;
+        bulk_g2s(dst + (m * Dt + s) * TA::PADF, src + s * d.is + (int64_t)m * d.im, 128u, &full[b], pol);
+      }
+    }
+  } else {
+    bool nonfinite = false;
+    for (int64_t k = 0;; ++k) {
+      const int b = (int)(k & 1);
+      mbar_wait(&full[b], (uint32_t)((k >> 1) & 1));
+      const long long pos = task_of[b];
+      if (pos < 0) break;
+      bool isB;
+      int64_t grp, sub;
+      decode_task(p, pos, isB, grp, sub);
+      V* buf = bufs + b * BUF;
+      if (!isB) {
+        TA::run_smem(p.a, p, grp, (int)sub, buf, twA, nonfinite, nullptr, nullptr);
+      } else {
+        const V* stg = (const V*)p.staging + (grp % p.nslots) * p.slot_elems + sub * p.b.it;
+        TB::run_smem(p.b, p, grp, (int)sub, buf, twB, nonfinite, p.doneB + grp, stg);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[b]);
+      if (!isB) {
+        TA::tsync();
+        if (TA::tx() == 0) {
+          __threadfence();
+          atomicAdd(p.doneA + grp, 1);
+        }
+      }
+    }
+    if (nonfinite) atomicOr(p.flag, 1);
+  }
 }
 
 }  // namespace efft

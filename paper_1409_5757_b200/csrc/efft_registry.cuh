@@ -16,17 +16,27 @@ struct KernelInfo {
 
 // Power-of-two tiles hold D*RHO = 512 points per column group, radix-3 tiles
 // 384; 256 threads; F columns of 128 bytes.
-template <typename R, int RHO> using PT = Tile<R, RHO, 512 / RHO, 256>;
-template <typename R, int RHO> using T3 = Tile<R, RHO, 384 / RHO, 256>;
+template <typename R, int RHO, bool MASK> using PT = Tile<R, RHO, 512 / RHO, 256, MASK, CT<R>::VEC>;
+template <typename R, int RHO, bool MASK> using T3 = Tile<R, RHO, 384 / RHO, 256, MASK, CT<R>::VEC>;
+// Consumer tiles of the warp-specialised staged kernel: 256 consumer threads
+// after the producer warp (TOFF 32), named barrier 1, one complex element per
+// lane access.
+template <typename R, int RHO> using ST = Tile<R, RHO, (RHO % 3 ? 512 : 384) / RHO, 256, false, 1, 32, 1>;
 
-template <typename R, class TA, class TB>
+template <typename R, class TA, class TB, bool WS = false>
 KernelInfo make_info() {
   using V = typename CT<R>::V;
   KernelInfo k{};
-  k.fn = pass_kernel<R, TA, TB>;
-  k.nt = TA::NT;
   const int sm = TA::SMEM_ELEMS > TB::SMEM_ELEMS ? TA::SMEM_ELEMS : TB::SMEM_ELEMS;
-  k.smem_bytes = (int)((sm + TA::RHO + TB::RHO) * sizeof(V));
+  if constexpr (WS) {
+    k.fn = staged_kernel<R, TA, TB>;
+    k.nt = TA::NT + 32;
+    k.smem_bytes = (int)((2 * sm + TA::RHO + TB::RHO) * sizeof(V));
+  } else {
+    k.fn = pass_kernel<R, TA, TB>;
+    k.nt = TA::NT;
+    k.smem_bytes = (int)((sm + TA::RHO + TB::RHO) * sizeof(V));
+  }
   k.rho_a = TA::RHO;
   k.d_a = TA::D;
   k.e_a = TA::E;

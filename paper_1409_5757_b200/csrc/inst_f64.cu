@@ -3,8 +3,8 @@
 
 namespace efft {
 
-#define D2(r) case r: *out = make_info<double, PT<double, r>, NoTile>(); return true;
-#define D3(r) case r: *out = make_info<double, T3<double, r>, NoTile>(); return true;
+#define D2(r) case r: *out = make_info<double, PT<double, r, true>, NoTile>(); return true;
+#define D3(r) case r: *out = make_info<double, T3<double, r, true>, NoTile>(); return true;
 bool get_direct_kernel_f64(int rho, KernelInfo* out) {
   switch (rho) {
     D2(2) D2(4) D2(8) D2(16) D2(32) D2(64) D2(128) D2(256) D2(512)
@@ -15,7 +15,7 @@ bool get_direct_kernel_f64(int rho, KernelInfo* out) {
 #undef D2
 #undef D3
 
-#define SA(rb) case rb: *out = make_info<double, Tile<double, RA, 1, 256>, PT<double, rb>>(); return true;
+#define SA(rb) case rb: *out = make_info<double, ST<double, RA>, ST<double, rb>, true>(); return true;
 template <int RA>
 static bool staged_f64(int rho_b, KernelInfo* out) {
   switch (rho_b) {
@@ -26,7 +26,7 @@ static bool staged_f64(int rho_b, KernelInfo* out) {
 #undef SA
 
 bool get_staged_kernel_f64(int rho_a, int rho_b, KernelInfo* out) {
-  if (rho_a == 512) return staged_f64<512>(rho_b, out);
+  if (rho_a == 256) return staged_f64<256>(rho_b, out);
   if (rho_a == 384) return staged_f64<384>(rho_b, out);
   return false;
 }
