@@ -11,6 +11,7 @@
 // all on the caller's stream.  Pass 1 reads `in` and writes `out`; pass 2 runs
 // in place on `out` (its tiles read every element they write before writing),
 // so the input is preserved (core.py:146-149) with just two device arrays.
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <cstdarg>
@@ -83,6 +84,7 @@ int fail(int code, const char* fmt, ...) {
   } while (0)
 
 struct PassPlan {
+  const void* tmA_ptr = nullptr;  // pointer the A tensor map was encoded for
   KernelInfo k;
   PassArgs args;
   int grid;
@@ -133,15 +135,18 @@ bool factor(int64_t n, int* M, int* t) {
 bool get_direct(int dtype, int rho, KernelInfo* k) {
   return dtype == EFFT_C64 ? efft::get_direct_kernel_f32(rho, k) : efft::get_direct_kernel_f64(rho, k);
 }
-bool get_staged(int dtype, int ra, int rb, KernelInfo* k) {
-  return dtype == EFFT_C64 ? efft::get_staged_kernel_f32(ra, rb, k)
-                           : efft::get_staged_kernel_f64(ra, rb, k);
-}
-
 int env_int(const char* name, int dflt) {
   const char* v = getenv(name);
   return v && *v ? atoi(v) : dflt;
 }
+
+bool get_staged(int dtype, int ra, int rb, KernelInfo* k) {
+  // EFFT_WS=1 selects the warp-specialised TMA kernel, 0 the register-path kernel
+  static const int ws = env_int("EFFT_WS", 0);
+  return dtype == EFFT_C64 ? efft::get_staged_kernel_f32(ra, rb, ws, k)
+                           : efft::get_staged_kernel_f64(ra, rb, ws, k);
+}
+
 
 // Decide direct vs staged and the sub-radices of one pass of radix R.
 bool pick_pass(int dtype, int64_t R, PassPlan* pp) {
@@ -158,12 +163,20 @@ bool pick_pass(int dtype, int64_t R, PassPlan* pp) {
   pp->rho_a = has3 ? 384 : 256;
   pp->rho_b = R / pp->rho_a;
   if (pp->rho_b * pp->rho_a != R || pp->rho_b > 512) return false;
-  // A tiles take D_A = tile/rho_a consecutive u (D_A | rho_b); B tiles cover
-  // D_B = 512/rho_b outputs k1 of the rho_a-point DFTs (D_B | rho_a)
-  const int64_t tile = has3 ? 384 : 512;
+  // complex64 power-of-two passes: EFFT_C64_TILE=256 selects 32 KB tiles (4 CTAs/SM)
+  static const int c64_tile = env_int("EFFT_C64_TILE", 512);
+  static const int ws = env_int("EFFT_WS", 0);
+  bool ok;
+  if (dtype == EFFT_C64 && !has3 && c64_tile == 256 && !ws && pp->rho_b <= 256)
+    ok = efft::get_staged_small_f32((int)pp->rho_b, &pp->k);
+  else
+    ok = get_staged(dtype, (int)pp->rho_a, (int)pp->rho_b, &pp->k);
+  if (!ok) return false;
+  // A tiles take D_A = tpts/rho_a consecutive u (D_A | rho_b); B tiles cover
+  // D_B = tpts/rho_b outputs k1 of the rho_a-point DFTs (D_B | rho_a)
+  const int64_t tile = pp->k.tpts;
   const int64_t da = tile / pp->rho_a;
-  if (pp->rho_b % da != 0 || pp->rho_b > tile || pp->rho_a % (tile / pp->rho_b) != 0) return false;
-  return get_staged(dtype, (int)pp->rho_a, (int)pp->rho_b, &pp->k);
+  return pp->rho_b % da == 0 && pp->rho_b <= tile && pp->rho_a % (tile / pp->rho_b) == 0;
 }
 
 SubDesc blank_desc() {
@@ -287,6 +300,59 @@ void describe_pass(efft_plan_s* pl, int p, int np, int64_t R, int64_t Ns) {
   a.total_tasks = a.ngroups * (A.ntasks + B.ntasks);
 }
 
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = (EncodeTiledFn)p;
+  }
+  return fn;
+}
+
+// TMA map of a staged pass's A tiles over its input: [column (uint64 units), u, t]
+int encode_A(efft_plan_s* pl, PassPlan& pp, const void* base) {
+  EncodeTiledFn enc = encode_fn();
+  if (!enc) return fail(EFFT_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  const int64_t N = pl->n, R = pp.radix, C = N / R, w = (int64_t)pl->elem / 8;
+  const int F = 128 / (int)pl->elem;
+  cuuint64_t dims[3] = {(cuuint64_t)(C * w), (cuuint64_t)pp.rho_b, (cuuint64_t)pp.rho_a};
+  cuuint64_t strides[2] = {(cuuint64_t)(C * pl->elem), (cuuint64_t)(pp.rho_b * C * pl->elem)};
+  cuuint32_t box[3] = {(cuuint32_t)(F * w), (cuuint32_t)pp.k.d_a, (cuuint32_t)(pp.rho_a > 256 ? pp.rho_a / 2 : pp.rho_a)};
+  cuuint32_t es[3] = {1, 1, 1};
+  CUresult r = enc(&pp.args.tmA, CU_TENSOR_MAP_DATA_TYPE_UINT64, 3, const_cast<void*>(base), dims, strides, box, es,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(EFFT_ERR_CUDA, "tensor map (A) encode failed: %d", (int)r);
+  pp.tmA_ptr = base;
+  return EFFT_OK;
+}
+
+// TMA map of a staged pass's B tiles over the staging ring: [f, k1, u, slot]
+int encode_B(efft_plan_s* pl, PassPlan& pp) {
+  EncodeTiledFn enc = encode_fn();
+  if (!enc) return fail(EFFT_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  const int64_t R = pp.radix, w = (int64_t)pl->elem / 8;
+  const int F = 128 / (int)pl->elem;
+  cuuint64_t dims[4] = {(cuuint64_t)(F * w), (cuuint64_t)pp.rho_a, (cuuint64_t)pp.rho_b, (cuuint64_t)pp.args.nslots};
+  cuuint64_t strides[3] = {(cuuint64_t)(F * pl->elem), (cuuint64_t)(pp.rho_a * F * pl->elem),
+                           (cuuint64_t)(R * F * pl->elem)};
+  cuuint32_t box[4] = {(cuuint32_t)(F * w), (cuuint32_t)pp.k.d_b,
+                       (cuuint32_t)(pp.rho_b > 256 ? pp.rho_b / 2 : pp.rho_b), 1};
+  cuuint32_t es[4] = {1, 1, 1, 1};
+  CUresult r = enc(&pp.args.tmB, CU_TENSOR_MAP_DATA_TYPE_UINT64, 4, pl->staging, dims, strides, box, es,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(EFFT_ERR_CUDA, "tensor map (B) encode failed: %d", (int)r);
+  return EFFT_OK;
+}
+
 int build_plan(efft_plan_s* pl) {
   int M, t;
   if (!factor(pl->n, &M, &t) || pl->n < 2)
@@ -359,6 +425,7 @@ int build_plan(efft_plan_s* pl) {
       if (slots < lag + 1) slots = lag + 1;
       if (slots > a.ngroups) slots = a.ngroups;
       a.lag = (int32_t)lag;
+      a.nowait = env_int("EFFT_DIAG_NOWAIT", 0);
       a.nslots = (int32_t)slots;
       size_t sb = (size_t)slots * a.slot_elems * pl->elem;
       if (sb > staging_bytes) staging_bytes = sb;
@@ -436,6 +503,15 @@ int efft_plan_create(efft_plan_t* out, int64_t n, int dtype, int direction, int 
   for (int p = 0; p < pl->npass; ++p) {
     PassArgs& a = pl->pass[p].args;
     a.staging = pl->staging;
+    if (pl->pass[p].staged && pl->pass[p].k.ws) {
+      int r2 = encode_B(pl, pl->pass[p]);
+      if (r2 != EFFT_OK) {
+        std::string keep = g_err;
+        efft_plan_destroy(pl);
+        g_err = keep;
+        return r2;
+      }
+    }
     a.task_counter = reinterpret_cast<unsigned long long*>(pl->counters + pl->pass[p].counter_off);
     a.doneA = pl->counters + pl->pass[p].counter_off + 2;
     a.doneB = a.doneA + a.ngroups;
@@ -497,10 +573,15 @@ int efft_execute(efft_plan_t pl, const void* d_in, void* d_out, void* stream) {
   CUDA_TRY(cudaMemsetAsync(pl->counters, 0, pl->counter_bytes, s));
   for (int p = 0; p < pl->npass; ++p) {
     if (pl->timing) CUDA_TRY(cudaEventRecord(pl->ev[p], s));
-    PassArgs a = pl->pass[p].args;
-    a.in = p == 0 ? d_in : d_out;
+    PassPlan& pp = pl->pass[p];
+    const void* src = p == 0 ? d_in : d_out;
+    if (pp.staged && pp.k.ws && pp.tmA_ptr != src) {
+      int rc = encode_A(pl, pp, src);
+      if (rc != EFFT_OK) return rc;
+    }
+    PassArgs a = pp.args;
+    a.in = src;
     a.out = d_out;
-    const PassPlan& pp = pl->pass[p];
     pp.k.fn<<<pp.grid, pp.k.nt, pp.k.smem_bytes, s>>>(a);
     CUDA_TRY(cudaGetLastError());
   }

@@ -24,6 +24,7 @@
 // rows padded to 144 B (16-byte aligned, conflict-free for row-, column- and
 // transposed accesses) between the in-CTA radix stages.
 #pragma once
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -184,6 +185,23 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
       : "memory");
 }
+// TMA tensor copies (one instruction per box), 128B-swizzled into shared memory
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, int c0, int c1, int c2,
+                                            uint64_t* bar, uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%2, %3, %4}], [%5], %6;" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar)), "l"(pol)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, int c0, int c1, int c2, int c3,
+                                            uint64_t* bar, uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%2, %3, %4, %5}], [%6], %7;" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_u32(bar)), "l"(pol)
+      : "memory");
+}
 // order generic-proxy writes observed through an acquire before async-proxy reads
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
 
@@ -318,11 +336,15 @@ struct PassArgs {
   SubDesc a, b;
   int64_t ngroups;
   int64_t total_tasks;
-  int32_t nslots, lag, staged, pad_;
+  int32_t nslots, lag, staged, nowait;  // nowait: diagnostic only (skips dependency waits)
   unsigned long long* task_counter;
   int32_t* doneA;
   int32_t* doneB;
   int32_t* flag;  // bit 0: non-finite input seen
+  // TMA maps of the warp-specialised staged kernel: A tiles read the pass
+  // input [column, u, t]; B tiles read the staging ring [f, k1, u, slot]
+  alignas(64) CUtensorMap tmA;
+  alignas(64) CUtensorMap tmB;
 };
 
 // e = A*C mod M for M = 2^k or 3*2^k (A, C >= 0), exact.
@@ -370,15 +392,16 @@ constexpr StagePlan make_stage_plan(int rho, int e) {
   return p;
 }
 
-template <typename R, int RHO_, int D_, int NT_, bool MASK_, int VEC_, int TOFF_ = 0, int BAR_ = 0>
+template <typename R, int RHO_, int D_, int NT_, bool MASK_, int VEC_, int TOFF_ = 0, int BAR_ = 0, bool SWZ_ = false>
 struct Tile {
   static constexpr int TOFF = TOFF_, BAR = BAR_;
+  static constexpr bool SWZ = SWZ_;  // stage-0 input lands as dense 128B-swizzled rows (TMA)
   // tile-thread index and the barrier over the tile's threads (named barrier
   // when the tile threads are the consumer warps of a warp-specialised CTA)
   __device__ __forceinline__ static int tx() { return (int)threadIdx.x - TOFF; }
   __device__ __forceinline__ static void tsync() {
     if constexpr (BAR == 0)
-      tsync();
+      __syncthreads();
     else
       asm volatile("bar.sync %0, %1;" ::"n"(BAR), "n"(NT_) : "memory");
   }
@@ -389,7 +412,8 @@ struct Tile {
   static constexpr bool MASK = MASK_;
   static constexpr int F = CT<R>::F;
   static constexpr int FV = F / VEC;     // lanes per 128-byte row (8)
-  static constexpr int PADF = F + 16 / (int)sizeof(V);  // smem row: 144 bytes, 16-byte aligned
+  static constexpr int EPC = 16 / (int)sizeof(V);       // elements per 16-byte chunk
+  static constexpr int PADF = F + EPC;                   // exchange row pitch: 144 bytes
   static constexpr int TILE = F * D * RHO;
   static constexpr int E = TILE / NT;    // complex elements per thread
   static constexpr int EV = E / VEC;     // butterfly elements per column-lane
@@ -400,7 +424,13 @@ struct Tile {
   static constexpr int NST = PL.n;
   static constexpr int SMEM_ELEMS = D * RHO * PADF;
 
+  // exchange layout: padded rows (index = base + t * const along m)
   __device__ __forceinline__ static int sidx(int f, int s, int m) { return (m * D + s) * PADF + f; }
+  // TMA landing layout: dense 128-byte rows, 16-byte chunks XOR-swizzled by row % 8
+  __device__ __forceinline__ static int sidx_in(int f, int s, int m) {
+    const int row = m * D + s;
+    return row * F + (((f / EPC) ^ (row & 7)) * EPC) + (f % EPC);
+  }
 
   // register position of output t of an S-point in-place DFT
   static constexpr int P(int S, int t) { return dif_pos(S, t); }
@@ -481,7 +511,7 @@ struct Tile {
     }
   }
 
-  template <int I>
+  template <int I, bool IN = false>
   __device__ __forceinline__ static void stage_read(V* v, const V* sm) {
     constexpr int S = PL.sig[I];
     constexpr int Q = EV / S;
@@ -490,9 +520,23 @@ struct Tile {
     for (int q = 0; q < Q; ++q) {
       int fv, u, s;
       coords<S>(q, fv, u, s);
+      if constexpr (IN) {
+        // swizzle term is t-invariant when L*D % 8 == 0: base + t * L*D*F
+        constexpr bool LIN = (L * D) % 8 == 0;
+        const int base = sidx_in(fv * VEC, s, u);
 #pragma unroll
-      for (int t = 0; t < S; ++t)
-        get(sm, fv * VEC, s, u + t * L, &v[(q * VEC) * S + t], &v[(q * VEC + VEC - 1) * S + t]);
+        for (int t = 0; t < S; ++t) {
+          const int ix = LIN ? base + t * L * D * F : sidx_in(fv * VEC, s, u + t * L);
+          if constexpr (VEC == 2)
+            unpack(*reinterpret_cast<const VT*>(sm + ix), &v[(q * VEC) * S + t], &v[(q * VEC + 1) * S + t]);
+          else
+            v[(q * VEC) * S + t] = sm[ix];
+        }
+      } else {
+#pragma unroll
+        for (int t = 0; t < S; ++t)
+          get(sm, fv * VEC, s, u + t * L, &v[(q * VEC) * S + t], &v[(q * VEC + VEC - 1) * S + t]);
+      }
     }
   }
 
@@ -677,6 +721,31 @@ struct Tile {
     constexpr int NO = TILE / W;
     const R sc = (R)d.scale;
     const uint64_t pol = policy_evict_first();
+    if constexpr (MODE == 1 && !MASK && NT % (D * F / W) == 0) {
+      // each thread owns fixed (f, s..s+W-1) and walks m with constant strides
+      constexpr int PER_M = D * F / W;  // outputs per m-plane
+      constexpr int MSTEP = NT / PER_M;
+      const int o = tx() * W;
+      const int s0 = o % D, f = (o / D) % F, m0 = o / (D * F);
+      V* ptr = dst + f * d.of + s0 * d.os + (int64_t)m0 * d.om;
+      const int64_t pstep = (int64_t)MSTEP * d.om;
+      const int ib = sidx(f, s0, m0);
+#pragma unroll 4
+      for (int it = 0; it < RHO / MSTEP; ++it) {
+        V y[W];
+#pragma unroll
+        for (int w = 0; w < W; ++w) {
+          y[w] = sm[ib + it * MSTEP * D * PADF + w * PADF];
+          if constexpr (CS) y[w] = mk(y[w].x * sc, -y[w].y * sc);
+        }
+        if constexpr (W == 2)
+          st_hint(reinterpret_cast<float4*>(ptr), pack(y[0], y[W - 1]), pol);
+        else
+          st_hint(ptr, y[0], pol);
+        ptr += pstep;
+      }
+      return;
+    }
 #pragma unroll 4
     for (int o0 = tx(); o0 < NO; o0 += NT) {
       const int o = o0 * W;
@@ -706,8 +775,7 @@ struct Tile {
   }
 
   __device__ __forceinline__ static void store(const SubDesc& d, const PassArgs& p, int64_t grp, int task,
-                                               const V* v, V* sm) {
-    const int64_t slot = d.out_staging ? grp % p.nslots : 0;
+                                               int slot, const V* v, V* sm) {
     V* dst = d.out_staging ? (V*)p.staging + slot * p.slot_elems + task * d.ot
                            : (V*)p.out + grp * d.og + task * d.ot;
     const bool cs = d.conj_out;
@@ -730,10 +798,9 @@ struct Tile {
   }
 
   // One tile: load (+conj, +finite check, +DIT twiddle), RHO-point DFTs, store.
-  __device__ static void run(const SubDesc& d, const PassArgs& p, int64_t grp, int task, V* sm,
+  __device__ static void run(const SubDesc& d, const PassArgs& p, int64_t grp, int task, int slot, V* sm,
                              const V* tw, bool& nonfinite, int32_t* release = nullptr) {
     V v[E];
-    const int64_t slot = d.in_staging ? grp % p.nslots : 0;
     const V* src = d.in_staging ? (const V*)p.staging + slot * p.slot_elems + task * d.it
                                 : (const V*)p.in + grp * d.ig + task * d.it;
     if (d.conj_in) {
@@ -765,7 +832,7 @@ struct Tile {
     } else {
       stages<0>(v, sm, tw);
     }
-    store(d, p, grp, task, v, sm);
+    store(d, p, grp, task, slot, v, sm);
   }
 
   __device__ __forceinline__ static void fixup(const SubDesc& d, V* v, bool& nonfinite) {
@@ -782,13 +849,13 @@ struct Tile {
   // the exchange buffer.  If `release` is set the rows came from the L2
   // staging ring at `stg`: they are discarded (no write-back) and the slot is
   // released to the producers of the next group.
-  __device__ static void run_smem(const SubDesc& d, const PassArgs& p, int64_t grp, int task, V* buf,
+  __device__ static void run_smem(const SubDesc& d, const PassArgs& p, int64_t grp, int task, int slot, V* buf,
                                   const V* tw, bool& nonfinite, int32_t* release, const V* stg) {
     V v[E];
     if (release != nullptr) {
       for (int r = tx(); r < D * RHO; r += NT) l2_discard(stg + (r % D) * d.is + (int64_t)(r / D) * d.im);
     }
-    stage_read<0>(v, buf);
+    stage_read<0, SWZ>(v, buf);
     tsync();  // every tile thread has its stage-0 data (and issued its discards)
     if (release != nullptr && tx() == 0) {
       __threadfence();
@@ -802,7 +869,7 @@ struct Tile {
       tsync();
       stages<1>(v, buf, tw);
     }
-    store(d, p, grp, task, v, buf);
+    store(d, p, grp, task, slot, v, buf);
   }
 };
 
@@ -817,79 +884,6 @@ __device__ __forceinline__ void wait_at_least(const int32_t* ctr, int32_t need) 
     __threadfence();
   }
   __syncthreads();
-}
-
-// Persistent pass kernel: CTAs pull tasks from one global counter in a fixed
-// order (A(0..lag-1), then B(g-lag), A(g) pairs, then the tail of B), which
-// makes every wait target a task that an already-running CTA owns.
-template <typename R, class TA, class TB>
-__global__ void __launch_bounds__(TA::NT, (TA::NT >= 512 ? 1 : 2)) pass_kernel(const __grid_constant__ PassArgs p) {
-  using V = typename CT<R>::V;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  constexpr int SM_ELEMS = TA::SMEM_ELEMS > TB::SMEM_ELEMS ? TA::SMEM_ELEMS : TB::SMEM_ELEMS;
-  V* sm = reinterpret_cast<V*>(smem_raw);
-  V* twA = sm + SM_ELEMS;
-  V* twB = twA + TA::RHO;
-  __shared__ unsigned long long s_task;
-  TA::build_table(twA);
-  if constexpr (TB::RHO > 0) TB::build_table(twB);
-  bool nonfinite = false;
-  if (threadIdx.x == 0) s_task = atomicAdd(p.task_counter, 1ull);
-  for (;;) {
-    __syncthreads();
-    const int64_t pos = (int64_t)s_task;
-    if (pos >= p.total_tasks) break;
-    // claim the next task now; its latency hides behind this task's work
-    // (deadlock-free: the smallest unfinished task is always a running one)
-    unsigned long long next = 0;
-    if (threadIdx.x == 0) next = atomicAdd(p.task_counter, 1ull);
-    if constexpr (TB::RHO == 0) {
-      const int64_t grp = pos / p.a.ntasks;
-      TA::run(p.a, p, grp, (int)(pos % p.a.ntasks), sm, twA, nonfinite);
-      __syncthreads();
-    } else {
-      const int64_t G = p.ngroups, L = p.lag, TAn = p.a.ntasks, TBn = p.b.ntasks;
-      bool isB;
-      int64_t grp, sub;
-      if (pos < L * TAn) {
-        isB = false;
-        grp = pos / TAn;
-        sub = pos % TAn;
-      } else if (pos < L * TAn + (G - L) * (TAn + TBn)) {
-        const int64_t q = pos - L * TAn;
-        const int64_t i = L + q / (TAn + TBn), r = q % (TAn + TBn);
-        if (r < TBn) {
-          isB = true;
-          grp = i - L;
-          sub = r;
-        } else {
-          isB = false;
-          grp = i;
-          sub = r - TBn;
-        }
-      } else {
-        const int64_t q = pos - L * TAn - (G - L) * (TAn + TBn);
-        isB = true;
-        grp = G - L + q / TBn;
-        sub = q % TBn;
-      }
-      if (!isB) {
-        if (grp >= p.nslots) wait_at_least(p.doneB + (grp - p.nslots), (int32_t)TBn);
-        TA::run(p.a, p, grp, (int)sub, sm, twA, nonfinite);
-        __syncthreads();
-        if (threadIdx.x == 0) {
-          __threadfence();
-          atomicAdd(p.doneA + grp, 1);
-        }
-      } else {
-        wait_at_least(p.doneA + grp, (int32_t)TAn);
-        TB::run(p.b, p, grp, (int)sub, sm, twB, nonfinite, p.doneB + grp);
-        __syncthreads();
-      }
-    }
-    if (threadIdx.x == 0) s_task = next;
-  }
-  if (__syncthreads_or(nonfinite) && threadIdx.x == 0) atomicOr(p.flag, 1);
 }
 
 // Task order of a staged pass: A(0..lag-1), then pairs [B(g-lag), A(g)], then
@@ -922,6 +916,79 @@ __device__ __forceinline__ void decode_task(const PassArgs& p, int64_t pos, bool
   }
 }
 
+// Persistent pass kernel: CTAs pull tasks from one global counter in a fixed
+// order (A(0..lag-1), then B(g-lag), A(g) pairs, then the tail of B), which
+// makes every wait target a task that an already-running CTA owns.
+// occupancy target: small (32 KB) tiles run 4 CTAs per SM, 64 KB tiles 2
+template <class TA> constexpr int min_blocks() { return TA::NT >= 512 ? 1 : (TA::TILE <= 4096 ? 4 : 2); }
+
+template <typename R, class TA, class TB>
+__global__ void __launch_bounds__(TA::NT, min_blocks<TA>()) pass_kernel(const __grid_constant__ PassArgs p) {
+  using V = typename CT<R>::V;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  constexpr int SM_ELEMS = TA::SMEM_ELEMS > TB::SMEM_ELEMS ? TA::SMEM_ELEMS : TB::SMEM_ELEMS;
+  V* sm = reinterpret_cast<V*>(smem_raw);
+  V* twA = sm + SM_ELEMS;
+  V* twB = twA + TA::RHO;
+  __shared__ long long s_pos, s_grp;
+  __shared__ int s_sub, s_slot, s_isB;
+  TA::build_table(twA);
+  if constexpr (TB::RHO > 0) TB::build_table(twB);
+  bool nonfinite = false;
+  // thread 0 claims and decodes tasks (one 64-bit division per task, not per thread)
+  auto publish = [&](unsigned long long pos) {
+    s_pos = (long long)pos;
+    if ((int64_t)pos >= p.total_tasks) return;
+    if constexpr (TB::RHO == 0) {
+      s_isB = 0;
+      s_grp = (long long)(pos / (unsigned long long)p.a.ntasks);
+      s_sub = (int)(pos % (unsigned long long)p.a.ntasks);
+      s_slot = 0;
+    } else {
+      bool isB;
+      int64_t grp, sub;
+      decode_task(p, (int64_t)pos, isB, grp, sub);
+      s_isB = isB;
+      s_grp = grp;
+      s_sub = (int)sub;
+      s_slot = (int)(grp % p.nslots);
+    }
+  };
+  if (threadIdx.x == 0) publish(atomicAdd(p.task_counter, 1ull));
+  for (;;) {
+    __syncthreads();
+    const long long pos = s_pos;
+    if (pos >= p.total_tasks) break;
+    const bool isB = s_isB;
+    const int64_t grp = s_grp;
+    const int sub = s_sub, slot = s_slot;
+    // claim the next task now; its latency hides behind this task's work
+    // (deadlock-free: the smallest unfinished task is always a running one)
+    unsigned long long next = 0;
+    if (threadIdx.x == 0) next = atomicAdd(p.task_counter, 1ull);
+    if constexpr (TB::RHO == 0) {
+      TA::run(p.a, p, grp, sub, slot, sm, twA, nonfinite);
+      __syncthreads();
+    } else {
+      if (!isB) {
+        if (grp >= p.nslots && !p.nowait) wait_at_least(p.doneB + (grp - p.nslots), p.b.ntasks);
+        TA::run(p.a, p, grp, sub, slot, sm, twA, nonfinite);
+        __syncthreads();
+        if (threadIdx.x == 0) {
+          __threadfence();
+          atomicAdd(p.doneA + grp, 1);
+        }
+      } else {
+        if (!p.nowait) wait_at_least(p.doneA + grp, p.a.ntasks);
+        TB::run(p.b, p, grp, sub, slot, sm, twB, nonfinite, p.doneB + grp);
+        __syncthreads();
+      }
+    }
+    if (threadIdx.x == 0) publish(next);
+  }
+  if (__syncthreads_or(nonfinite) && threadIdx.x == 0) atomicOr(p.flag, 1);
+}
+
 // Warp-specialised staged pass (one CTA per SM, persistent).
 //   warp 0 (producer): claims tasks in order, resolves their dependency, and
 //     copies the tile's 128-byte rows (HBM input for A tasks, the L2 staging
@@ -933,17 +1000,20 @@ __device__ __forceinline__ void decode_task(const PassArgs& p, int64_t pos, bool
 //     then release the buffer (empty mbarrier) and, for A tasks, publish the
 //     group counter.
 template <typename R, class TA, class TB>
-__global__ void __launch_bounds__(TA::NT + 32, 1) staged_kernel(const __grid_constant__ PassArgs p) {
+__global__ void __launch_bounds__(TA::NT + 32, 1) staged_kernel(const __grid_constant__ PassArgs p) {  // NOLINT
   using V = typename CT<R>::V;
   static_assert(TA::NT == TB::NT && TA::TOFF == 32 && TB::TOFF == 32, "consumer warps follow warp 0");
-  static_assert(TA::PADF == TB::PADF, "same row pitch");
+  static_assert(TA::SWZ && TB::SWZ, "TMA tiles land 128B-swizzled");
   extern __shared__ __align__(128) unsigned char smem_raw[];
   constexpr int BUF = TA::SMEM_ELEMS > TB::SMEM_ELEMS ? TA::SMEM_ELEMS : TB::SMEM_ELEMS;
-  V* bufs = reinterpret_cast<V*>(smem_raw);
+  static_assert((BUF * sizeof(V)) % 1024 == 0, "swizzled buffers stay 1024-byte aligned");
+  // 128B swizzle needs 1024-byte aligned buffers (the launch adds 1 KB slack)
+  V* bufs = reinterpret_cast<V*>(smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u));
   V* twA = bufs + 2 * BUF;
   V* twB = twA + TA::RHO;
   __shared__ __align__(8) uint64_t full[2], empty[2];
-  __shared__ long long task_of[2];
+  __shared__ long long task_of[2], task_grp[2];
+  __shared__ int task_sub[2], task_slot[2], task_isB[2];
   if (threadIdx.x == 0) {
     mbar_init(&full[0], 1);
     mbar_init(&full[1], 1);
@@ -976,26 +1046,38 @@ __global__ void __launch_bounds__(TA::NT + 32, 1) staged_kernel(const __grid_con
       if (lane == 0) {
         const int32_t* ctr = isB ? p.doneA + grp : (grp >= p.nslots ? p.doneB + (grp - p.nslots) : nullptr);
         const int32_t need = isB ? p.a.ntasks : p.b.ntasks;
-        if (ctr != nullptr) {
+        if (ctr != nullptr && !p.nowait) {
           while (*(volatile const int32_t*)ctr < need) __nanosleep(32);
           __threadfence();
         }
         fence_proxy_async();
         task_of[b] = (long long)pos;
+        task_grp[b] = grp;
+        task_sub[b] = (int)sub;
+        task_slot[b] = (int)(grp % p.nslots);
+        task_isB[b] = isB;
         const int rows = isB ? TB::D * TB::RHO : TA::D * TA::RHO;
         mbar_arrive_tx(&full[b], (uint32_t)rows * 128u);
       }
       __syncwarp();
-      const SubDesc& d = isB ? p.b : p.a;
-      const int Dt = isB ? TB::D : TA::D;
-      const int rows = isB ? TB::D * TB::RHO : TA::D * TA::RHO;
-      const V* src = d.in_staging ? (const V*)p.staging + (grp % p.nslots) * p.slot_elems + sub * d.it
-                                  : (const V*)p.in + grp * d.ig + sub * d.it;
-      V* dst = bufs + b * BUF;
-      for (int r = lane; r < rows; r += 32) {
-        const int s = r % Dt, m = r / Dt;
-        bulk_g2s(dst + (m * Dt + s) * TA::PADF, src + s * d.is + (int64_t)m * d.im, 128u, &full[b], pol);
+      if (lane == 0) {
+        V* dst = bufs + b * BUF;
+        if (!isB) {
+          constexpr int W = (int)sizeof(V) / 8;  // tensor-map units (uint64) per element
+          constexpr int BOX = TA::RHO > 256 ? TA::RHO / 2 : TA::RHO;
+#pragma unroll
+          for (int h = 0; h < TA::RHO / BOX; ++h)
+            tma_load_3d(dst + h * BOX * TA::D * TA::F, &p.tmA, (int)(grp * TA::F * W), (int)(sub * TA::D),
+                        h * BOX, &full[b], pol);
+        } else {
+          constexpr int BOX = TB::RHO > 256 ? TB::RHO / 2 : TB::RHO;
+#pragma unroll
+          for (int h = 0; h < TB::RHO / BOX; ++h)
+            tma_load_4d(dst + h * BOX * TB::D * TB::F, &p.tmB, 0, (int)(sub * TB::D), h * BOX, task_slot[b],
+                        &full[b], pol);
+        }
       }
+      __syncwarp();
     }
   } else {
     bool nonfinite = false;
@@ -1004,15 +1086,15 @@ __global__ void __launch_bounds__(TA::NT + 32, 1) staged_kernel(const __grid_con
       mbar_wait(&full[b], (uint32_t)((k >> 1) & 1));
       const long long pos = task_of[b];
       if (pos < 0) break;
-      bool isB;
-      int64_t grp, sub;
-      decode_task(p, pos, isB, grp, sub);
+      const bool isB = task_isB[b];
+      const int64_t grp = task_grp[b];
+      const int sub = task_sub[b], slot = task_slot[b];
       V* buf = bufs + b * BUF;
       if (!isB) {
-        TA::run_smem(p.a, p, grp, (int)sub, buf, twA, nonfinite, nullptr, nullptr);
+        TA::run_smem(p.a, p, grp, sub, slot, buf, twA, nonfinite, nullptr, nullptr);
       } else {
-        const V* stg = (const V*)p.staging + (grp % p.nslots) * p.slot_elems + sub * p.b.it;
-        TB::run_smem(p.b, p, grp, (int)sub, buf, twB, nonfinite, p.doneB + grp, stg);
+        const V* stg = (const V*)p.staging + (int64_t)slot * p.slot_elems + (int64_t)sub * p.b.it;
+        TB::run_smem(p.b, p, grp, sub, slot, buf, twB, nonfinite, p.doneB + grp, stg);
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[b]);

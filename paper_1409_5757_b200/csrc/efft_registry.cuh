@@ -12,6 +12,8 @@ struct KernelInfo {
   int rho_b, d_b, e_b;
   int stages_a[12], nst_a;
   int stages_b[12], nst_b;
+  int ws;    // warp-specialised TMA kernel (needs tensor maps)
+  int tpts;  // D * RHO of the tiles (points per column group per task)
 };
 
 // Power-of-two tiles hold D*RHO = 512 points per column group, radix-3 tiles
@@ -21,7 +23,7 @@ template <typename R, int RHO, bool MASK> using T3 = Tile<R, RHO, 384 / RHO, 256
 // Consumer tiles of the warp-specialised staged kernel: 256 consumer threads
 // after the producer warp (TOFF 32), named barrier 1, one complex element per
 // lane access.
-template <typename R, int RHO> using ST = Tile<R, RHO, (RHO % 3 ? 512 : 384) / RHO, 256, false, 1, 32, 1>;
+template <typename R, int RHO> using ST = Tile<R, RHO, (RHO % 3 ? 512 : 384) / RHO, 256, false, 1, 32, 1, true>;
 
 template <typename R, class TA, class TB, bool WS = false>
 KernelInfo make_info() {
@@ -31,7 +33,8 @@ KernelInfo make_info() {
   if constexpr (WS) {
     k.fn = staged_kernel<R, TA, TB>;
     k.nt = TA::NT + 32;
-    k.smem_bytes = (int)((2 * sm + TA::RHO + TB::RHO) * sizeof(V));
+    k.smem_bytes = (int)((2 * sm + TA::RHO + TB::RHO) * sizeof(V)) + 1024;  // + swizzle alignment slack
+    k.ws = 1;
   } else {
     k.fn = pass_kernel<R, TA, TB>;
     k.nt = TA::NT;
@@ -39,6 +42,7 @@ KernelInfo make_info() {
   }
   k.rho_a = TA::RHO;
   k.d_a = TA::D;
+  k.tpts = TA::D * TA::RHO;
   k.e_a = TA::E;
   k.nst_a = TA::NST;
   for (int i = 0; i < TA::NST; ++i) k.stages_a[i] = TA::PL.sig[i];
@@ -55,7 +59,8 @@ KernelInfo make_info() {
 // Defined in inst_f32.cu / inst_f64.cu.
 bool get_direct_kernel_f32(int rho, KernelInfo* out);
 bool get_direct_kernel_f64(int rho, KernelInfo* out);
-bool get_staged_kernel_f32(int rho_a, int rho_b, KernelInfo* out);
-bool get_staged_kernel_f64(int rho_a, int rho_b, KernelInfo* out);
+bool get_staged_kernel_f32(int rho_a, int rho_b, int ws, KernelInfo* out);
+bool get_staged_kernel_f64(int rho_a, int rho_b, int ws, KernelInfo* out);
+bool get_staged_small_f32(int rho_b, KernelInfo* out);
 
 }  // namespace efft

@@ -15,7 +15,9 @@ bool get_direct_kernel_f32(int rho, KernelInfo* out) {
 #undef D2
 #undef D3
 
-#define SA(rb) case rb: *out = make_info<float, ST<float, RA>, ST<float, rb>, true>(); return true;
+// complex64 warp-specialised tiles: 16 consumer warps, 16 elements per thread
+template <int RHO> using ST16 = Tile<float, RHO, (RHO % 3 ? 512 : 384) / RHO, 512, false, 1, 32, 1, true>;
+#define SA(rb) case rb: *out = make_info<float, ST16<RA>, ST16<rb>, true>(); return true;
 template <int RA>
 static bool staged_f32(int rho_b, KernelInfo* out) {
   switch (rho_b) {
@@ -25,9 +27,37 @@ static bool staged_f32(int rho_b, KernelInfo* out) {
 }
 #undef SA
 
-bool get_staged_kernel_f32(int rho_a, int rho_b, KernelInfo* out) {
-  if (rho_a == 256) return staged_f32<256>(rho_b, out);
-  if (rho_a == 384) return staged_f32<384>(rho_b, out);
+// register-path staged variants (persistent pass_kernel, no TMA)
+#define SR(rb) case rb: *out = make_info<float, Tile<float, RA, (RA % 3 ? 512 : 384) / RA, 256, false, CT<float>::VEC>, PT<float, rb, false>>(); return true;
+template <int RA>
+static bool staged_reg_f32(int rho_b, KernelInfo* out) {
+  switch (rho_b) {
+    SR(2) SR(4) SR(8) SR(16) SR(32) SR(64) SR(128) SR(256) SR(512)
+    default: return false;
+  }
+}
+#undef SR
+
+// 32 KB complex64 tiles: 256 points per column group, 16 elements per thread,
+// radix-16 stages, 4 CTAs (32 warps) per SM
+template <int RHO> using SM32 = Tile<float, RHO, 256 / RHO, 256, false, 1>;
+#define SS(rb) case rb: *out = make_info<float, SM32<256>, SM32<rb>>(); return true;
+bool get_staged_small_f32(int rho_b, KernelInfo* out) {
+  switch (rho_b) {
+    SS(2) SS(4) SS(8) SS(16) SS(32) SS(64) SS(128) SS(256)
+    default: return false;
+  }
+}
+#undef SS
+
+bool get_staged_kernel_f32(int rho_a, int rho_b, int ws, KernelInfo* out) {
+  if (ws) {
+    if (rho_a == 256) return staged_f32<256>(rho_b, out);
+    if (rho_a == 384) return staged_f32<384>(rho_b, out);
+  } else {
+    if (rho_a == 256) return staged_reg_f32<256>(rho_b, out);
+    if (rho_a == 384) return staged_reg_f32<384>(rho_b, out);
+  }
   return false;
 }
 

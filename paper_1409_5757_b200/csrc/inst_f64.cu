@@ -25,9 +25,25 @@ static bool staged_f64(int rho_b, KernelInfo* out) {
 }
 #undef SA
 
-bool get_staged_kernel_f64(int rho_a, int rho_b, KernelInfo* out) {
-  if (rho_a == 256) return staged_f64<256>(rho_b, out);
-  if (rho_a == 384) return staged_f64<384>(rho_b, out);
+// register-path staged variants (persistent pass_kernel, no TMA)
+#define SR(rb) case rb: *out = make_info<double, Tile<double, RA, (RA % 3 ? 512 : 384) / RA, 256, false, CT<double>::VEC>, PT<double, rb, false>>(); return true;
+template <int RA>
+static bool staged_reg_f64(int rho_b, KernelInfo* out) {
+  switch (rho_b) {
+    SR(2) SR(4) SR(8) SR(16) SR(32) SR(64) SR(128) SR(256) SR(512)
+    default: return false;
+  }
+}
+#undef SR
+
+bool get_staged_kernel_f64(int rho_a, int rho_b, int ws, KernelInfo* out) {
+  if (ws) {
+    if (rho_a == 256) return staged_f64<256>(rho_b, out);
+    if (rho_a == 384) return staged_f64<384>(rho_b, out);
+  } else {
+    if (rho_a == 256) return staged_reg_f64<256>(rho_b, out);
+    if (rho_a == 384) return staged_reg_f64<384>(rho_b, out);
+  }
   return false;
 }
 
