@@ -17,6 +17,10 @@
  *                            run_transform(h); h.result` does end to end)
  *   efft_plan_destroy     <- TransformHandle.close()                          core.py:172-174
  *   efft_nonfinite_seen   <- scatter()'s non-finite input check               scatter.py:38-39
+ *   efft_plan_create_columns, efft_permute_swap01/12
+ *                         <- one recursion level of process_and_reassemble
+ *                            (recombine.py:263-295) as a batched column pass +
+ *                            the all-to-all packing of the sharded six-step
  *   efft_last_error       <- the exception message of errors.py:4-45
  *
  * Status codes map 1:1 onto the reference exception classes (errors.py).
@@ -51,7 +55,8 @@ extern "C" {
 #define EFFT_INVERSE (+1) /* exp(+2 pi i k n / N), scaled by 1/N               */
 
 /* flags for efft_plan_create */
-#define EFFT_FLAG_CHECK_FINITE 0x1u /* detect non-finite input inside pass 1 */
+#define EFFT_FLAG_CHECK_FINITE 0x1u  /* detect non-finite input inside pass 1 */
+#define EFFT_FLAG_SCALE_INVERSE 0x2u /* column plans: scale the inverse by 1/len */
 
 typedef struct efft_plan_s *efft_plan_t;
 
@@ -92,6 +97,25 @@ int efft_plan_destroy(efft_plan_t plan);
  * durations of the most recent execution. */
 int efft_plan_enable_timing(efft_plan_t plan, int enable);
 int efft_plan_launch_times(efft_plan_t plan, float *ms, int max_launches);
+
+/* Batched column transform (one HBM pass), the local step of the sharded
+ * six-step (reference counterpart: the per-bin leaf + merge work of one
+ * recursion level, leaf_dft.py:93-125 / recombine.py:216-260, batched).
+ * For every column c < cols of a row-major (len x cols) array:
+ *   out[c + k*cols] = sum_r in[c + r*cols] * W_tw^((tw_offset + c) * r) * W_len^(r*k)
+ * W_m = exp(direction * 2 pi i / m); tw_mod = 0 disables the twiddle.  Inverse
+ * is unscaled unless EFFT_FLAG_SCALE_INVERSE.  len <= 2^17 (one pass); in ==
+ * out is allowed. */
+int efft_plan_create_columns(efft_plan_t *plan, int64_t len, int64_t cols, int dtype, int direction,
+                             int device, int64_t tw_mod, int64_t tw_offset, uint32_t flags);
+
+/* Block permutations (all-to-all packing): shapes (n0, n1, n2) of 8- or
+ * 16-byte elements.  swap01: out[b][a][c] = in[a][b][c];  swap12:
+ * out[a][c][b] = in[a][b][c].  Asynchronous on `stream`; in != out. */
+int efft_permute_swap01(const void *in, void *out, int64_t n0, int64_t n1, int64_t n2, int elem_bytes,
+                        void *stream);
+int efft_permute_swap12(const void *in, void *out, int64_t n0, int64_t n1, int64_t n2, int elem_bytes,
+                        void *stream);
 
 const char *efft_last_error(void);
 int efft_version(void);

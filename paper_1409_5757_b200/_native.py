@@ -19,6 +19,7 @@ EFFT_R32 = 3
 EFFT_FORWARD = -1
 EFFT_INVERSE = 1
 EFFT_FLAG_CHECK_FINITE = 0x1
+EFFT_FLAG_SCALE_INVERSE = 0x2
 
 # status code -> exception class (include/efft_b200.h, reference errors.py)
 _STATUS = {
@@ -44,6 +45,9 @@ EXPORTED = (
     "efft_nonfinite_seen",
     "efft_plan_destroy",
     "efft_plan_enable_timing",
+    "efft_plan_create_columns",
+    "efft_permute_swap01",
+    "efft_permute_swap12",
     "efft_plan_launch_times",
     "efft_last_error",
     "efft_version",
@@ -75,6 +79,9 @@ def load():
     lib.efft_nonfinite_seen.argtypes = [vp, ctypes.POINTER(i32), vp]
     lib.efft_plan_destroy.argtypes = [vp]
     lib.efft_plan_enable_timing.argtypes = [vp, i32]
+    lib.efft_plan_create_columns.argtypes = [ctypes.POINTER(vp), i64, i64, i32, i32, i32, i64, i64, u32]
+    lib.efft_permute_swap01.argtypes = [vp, vp, i64, i64, i64, i32, vp]
+    lib.efft_permute_swap12.argtypes = [vp, vp, i64, i64, i64, i32, vp]
     lib.efft_plan_launch_times.argtypes = [vp, ctypes.POINTER(ctypes.c_float), i32]
     lib.efft_last_error.restype = ctypes.c_char_p
     lib.efft_last_error.argtypes = []
@@ -94,14 +101,29 @@ def check(rc: int, what: str = "") -> None:
     raise exc(f"{what}: {msg}" if what else msg)
 
 
+def permute_swap01(d_in: int, d_out: int, n0: int, n1: int, n2: int, elem: int, stream: int) -> None:
+    check(load().efft_permute_swap01(d_in, d_out, n0, n1, n2, elem, stream), "efft_permute_swap01")
+
+
+def permute_swap12(d_in: int, d_out: int, n0: int, n1: int, n2: int, elem: int, stream: int) -> None:
+    check(load().efft_permute_swap12(d_in, d_out, n0, n1, n2, elem, stream), "efft_permute_swap12")
+
+
 class NativePlan:
     """Owns one efft_plan_t."""
 
-    def __init__(self, n: int, dtype: int, direction: int, device: int, flags: int = 0):
+    def __init__(self, n: int, dtype: int, direction: int, device: int, flags: int = 0, *,
+                 columns=None):
         lib = load()
         h = ctypes.c_void_p()
-        check(lib.efft_plan_create(ctypes.byref(h), n, dtype, direction, device, flags),
-              "efft_plan_create")
+        if columns is None:
+            check(lib.efft_plan_create(ctypes.byref(h), n, dtype, direction, device, flags),
+                  "efft_plan_create")
+        else:
+            cols, tw_mod, tw_offset = columns
+            check(lib.efft_plan_create_columns(ctypes.byref(h), n, cols, dtype, direction, device,
+                                               tw_mod, tw_offset, flags),
+                  "efft_plan_create_columns")
         self._h = h
         self.n, self.dtype, self.direction, self.device = n, dtype, direction, device
 

@@ -17,6 +17,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
+#include <algorithm>
 #include <cstring>
 #include <string>
 
@@ -100,6 +101,9 @@ struct efft_plan_s {
   int64_t n;        // complex length the passes run on (n_user / 2 for EFFT_R32)
   int64_t n_user;
   bool real_input = false;
+  // batched column plan (efft_plan_create_columns): one pass, column store
+  bool columns = false;
+  int64_t col_len = 0, col_count = 0, col_tw_mod = 0, col_tw_offset = 0;
   int dtype, direction, device;
   uint32_t flags;
   int npass;
@@ -169,6 +173,14 @@ bool pick_pass(int dtype, int64_t R, PassPlan* pp) {
   bool ok;
   if (dtype == EFFT_C64 && !has3 && c64_tile == 256 && !ws && pp->rho_b <= 256)
     ok = efft::get_staged_small_f32((int)pp->rho_b, &pp->k);
+  else if (dtype == EFFT_C64 && !has3 && c64_tile == 1 && !ws && pp->rho_b >= 8 && pp->rho_b <= 256)
+    ok = efft::get_staged_wide_f32((int)pp->rho_b, &pp->k);
+  else if (!has3 && c64_tile == 3 && !ws && pp->rho_b >= 8 && pp->rho_b <= 256)
+    ok = dtype == EFFT_C64 ? efft::get_staged_tp_f32((int)pp->rho_b, &pp->k)
+                           : efft::get_staged_tp_f64((int)pp->rho_b, &pp->k);
+  else if (!has3 && c64_tile == 2 && !ws && pp->rho_b >= 8 && pp->rho_b <= 256)
+    ok = dtype == EFFT_C64 ? efft::get_staged_pf_f32((int)pp->rho_b, &pp->k)
+                           : efft::get_staged_pf_f64((int)pp->rho_b, &pp->k);
   else
     ok = get_staged(dtype, (int)pp->rho_a, (int)pp->rho_b, &pp->k);
   if (!ok) return false;
@@ -355,13 +367,27 @@ int encode_B(efft_plan_s* pl, PassPlan& pp) {
 
 int build_plan(efft_plan_s* pl) {
   int M, t;
-  if (!factor(pl->n, &M, &t) || pl->n < 2)
+  if (pl->columns) {
+    if (!factor(pl->col_len, &M, &t) || pl->col_len < 2)
+      return fail(EFFT_ERR_UNSUPPORTED_SIZE, "len=%lld is not M*2^t with M in {1,3}", (long long)pl->col_len);
+  } else if (!factor(pl->n, &M, &t) || pl->n < 2)
     return fail(EFFT_ERR_UNSUPPORTED_SIZE,
                 "n=%lld is not M*2^t with M in {1,3} and n >= 2", (long long)pl->n);
   const int dt = pl->dtype;
   int64_t R1, R2;
   const int64_t dmax = M == 3 ? 384 : 512;
-  if (pl->n <= dmax) {
+  if (pl->columns) {
+    pl->npass = 1;
+    R1 = pl->col_len;
+    R2 = 1;
+    PassPlan a;
+    if (!pick_pass(dt, R1, &a))
+      return fail(EFFT_ERR_UNSUPPORTED_SIZE, "no single-pass kernel for len=%lld", (long long)R1);
+    const int F = dt == EFFT_C64 ? 16 : 8;
+    if (a.staged && pl->col_count % F)
+      return fail(EFFT_ERR_UNSUPPORTED_SIZE, "cols=%lld must be a multiple of %d for len=%lld",
+                  (long long)pl->col_count, F, (long long)R1);
+  } else if (pl->n <= dmax) {
     pl->npass = 1;
     R1 = pl->n;
     R2 = 1;
@@ -400,7 +426,16 @@ int build_plan(efft_plan_s* pl) {
     PassPlan& pp = pl->pass[p];
     if (!pick_pass(dt, radices[p], &pp))
       return fail(EFFT_ERR_UNSUPPORTED_SIZE, "no kernel for radix %lld", (long long)radices[p]);
-    describe_pass(pl, p, pl->npass, radices[p], ns);
+    describe_pass(pl, p, pl->npass, radices[p], pl->columns ? pl->col_count : ns);
+    if (pl->columns) {  // column store (Ns = cols), caller-chosen twiddle, unscaled inverse
+      SubDesc& d = pp.staged ? pp.args.a : pp.args.a;
+      const bool inverse = pl->direction == EFFT_INVERSE;
+      SubDesc& last = pp.staged ? pp.args.b : pp.args.a;
+      d.tw_mod = pl->col_tw_mod;
+      d.A0 = pl->col_tw_offset;
+      last.scale = (inverse && (pl->flags & EFFT_FLAG_SCALE_INVERSE)) ? 1.0 / (double)pl->col_len : 1.0;
+      (void)inverse;
+    }
     ns *= radices[p];
     CUDA_TRY(cudaFuncSetAttribute(pp.k.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, pp.k.smem_bytes));
     int occ = 0;
@@ -425,7 +460,7 @@ int build_plan(efft_plan_s* pl) {
       if (slots < lag + 1) slots = lag + 1;
       if (slots > a.ngroups) slots = a.ngroups;
       a.lag = (int32_t)lag;
-      a.nowait = env_int("EFFT_DIAG_NOWAIT", 0);
+      a.nowait = env_int("EFFT_DIAG_NOWAIT", 0);  // diagnostics: 1 skip waits, 2 skip DFT work
       a.nslots = (int32_t)slots;
       size_t sb = (size_t)slots * a.slot_elems * pl->elem;
       if (sb > staging_bytes) staging_bytes = sb;
@@ -444,41 +479,8 @@ int build_plan(efft_plan_s* pl) {
 
 }  // namespace
 
-extern "C" {
-
-int efft_version(void) { return 1; }
-
-const char* efft_last_error(void) { return g_err.c_str(); }
-
-int efft_plan_create(efft_plan_t* out, int64_t n, int dtype, int direction, int device,
-                     uint32_t flags) {
-  if (!out) return fail(EFFT_ERR_INVALID_ARG, "plan pointer is NULL");
-  *out = nullptr;
-  if (dtype != EFFT_C64 && dtype != EFFT_C128 && dtype != EFFT_R32)
-    return fail(EFFT_ERR_INVALID_ARG, "dtype %d", dtype);
-  if (dtype == EFFT_R32 && direction != EFFT_FORWARD)
-    return fail(EFFT_ERR_INVALID_ARG, "the real-input path is forward only");
-  if (dtype == EFFT_R32 && (n < 4 || (n & 1)))
-    return fail(EFFT_ERR_UNSUPPORTED_SIZE, "real-input n must be even and >= 4, got %lld", (long long)n);
-  if (direction != EFFT_FORWARD && direction != EFFT_INVERSE)
-    return fail(EFFT_ERR_INVALID_ARG, "direction must be -1 or +1, got %d", direction);
-  if (n < 1) return fail(EFFT_ERR_INVALID_ARG, "n must be >= 1");
-  int ndev = 0;
-  CUDA_TRY(cudaGetDeviceCount(&ndev));
-  if (device < 0 || device >= ndev) return fail(EFFT_ERR_INVALID_ARG, "device %d of %d", device, ndev);
-  CUDA_TRY(cudaSetDevice(device));
-  efft_plan_s* pl = new efft_plan_s();
-  pl->n_user = n;
-  pl->real_input = dtype == EFFT_R32;
-  pl->n = pl->real_input ? n / 2 : n;
-  if (pl->real_input) dtype = EFFT_C64;
-  pl->dtype = dtype;
-  pl->direction = direction;
-  pl->device = device;
-  pl->flags = flags;
-  pl->elem = dtype == EFFT_C64 ? 8 : 16;
-  cudaDeviceGetAttribute(&pl->num_sms, cudaDevAttrMultiProcessorCount, device);
-  int rc = build_plan(pl);
+int finish_plan(efft_plan_s* pl) {
+  int rc = EFFT_OK;
   if (rc == EFFT_OK && pl->staging_bytes) {
     if (cudaMalloc(&pl->staging, pl->staging_bytes) != cudaSuccess) {
       cudaGetLastError();
@@ -517,7 +519,119 @@ int efft_plan_create(efft_plan_t* out, int64_t n, int dtype, int direction, int 
     a.doneB = a.doneA + a.ngroups;
     a.flag = pl->flag;
   }
+  return EFFT_OK;
+}
+
+extern "C" {
+
+int efft_version(void) { return 1; }
+
+const char* efft_last_error(void) { return g_err.c_str(); }
+
+int efft_plan_create(efft_plan_t* out, int64_t n, int dtype, int direction, int device,
+                     uint32_t flags) {
+  if (!out) return fail(EFFT_ERR_INVALID_ARG, "plan pointer is NULL");
+  *out = nullptr;
+  if (dtype != EFFT_C64 && dtype != EFFT_C128 && dtype != EFFT_R32)
+    return fail(EFFT_ERR_INVALID_ARG, "dtype %d", dtype);
+  if (dtype == EFFT_R32 && direction != EFFT_FORWARD)
+    return fail(EFFT_ERR_INVALID_ARG, "the real-input path is forward only");
+  if (dtype == EFFT_R32 && (n < 4 || (n & 1)))
+    return fail(EFFT_ERR_UNSUPPORTED_SIZE, "real-input n must be even and >= 4, got %lld", (long long)n);
+  if (direction != EFFT_FORWARD && direction != EFFT_INVERSE)
+    return fail(EFFT_ERR_INVALID_ARG, "direction must be -1 or +1, got %d", direction);
+  if (n < 1) return fail(EFFT_ERR_INVALID_ARG, "n must be >= 1");
+  int ndev = 0;
+  CUDA_TRY(cudaGetDeviceCount(&ndev));
+  if (device < 0 || device >= ndev) return fail(EFFT_ERR_INVALID_ARG, "device %d of %d", device, ndev);
+  CUDA_TRY(cudaSetDevice(device));
+  efft_plan_s* pl = new efft_plan_s();
+  pl->n_user = n;
+  pl->real_input = dtype == EFFT_R32;
+  pl->n = pl->real_input ? n / 2 : n;
+  if (pl->real_input) dtype = EFFT_C64;
+  pl->dtype = dtype;
+  pl->direction = direction;
+  pl->device = device;
+  pl->flags = flags;
+  pl->elem = dtype == EFFT_C64 ? 8 : 16;
+  cudaDeviceGetAttribute(&pl->num_sms, cudaDevAttrMultiProcessorCount, device);
+  int rc = build_plan(pl);
+  if (rc != EFFT_OK) {
+    delete pl;
+    return rc;
+  }
+  rc = finish_plan(pl);  // frees the plan itself on failure
+  if (rc != EFFT_OK) return rc;
   *out = pl;
+  return EFFT_OK;
+}
+
+int efft_plan_create_columns(efft_plan_t* out, int64_t len, int64_t cols, int dtype, int direction, int device,
+                             int64_t tw_mod, int64_t tw_offset, uint32_t flags) {
+  if (!out) return fail(EFFT_ERR_INVALID_ARG, "plan pointer is NULL");
+  *out = nullptr;
+  if (dtype != EFFT_C64 && dtype != EFFT_C128) return fail(EFFT_ERR_INVALID_ARG, "dtype %d", dtype);
+  if (direction != EFFT_FORWARD && direction != EFFT_INVERSE)
+    return fail(EFFT_ERR_INVALID_ARG, "direction must be -1 or +1, got %d", direction);
+  if (len < 2 || cols < 2) return fail(EFFT_ERR_INVALID_ARG, "len and cols must be >= 2");
+  if (tw_mod < 0 || tw_offset < 0) return fail(EFFT_ERR_INVALID_ARG, "negative twiddle parameters");
+  int ndev = 0;
+  CUDA_TRY(cudaGetDeviceCount(&ndev));
+  if (device < 0 || device >= ndev) return fail(EFFT_ERR_INVALID_ARG, "device %d of %d", device, ndev);
+  CUDA_TRY(cudaSetDevice(device));
+  efft_plan_s* pl = new efft_plan_s();
+  pl->columns = true;
+  pl->col_len = len;
+  pl->col_count = cols;
+  pl->col_tw_mod = tw_mod;
+  pl->col_tw_offset = tw_offset;
+  pl->n = pl->n_user = len * cols;
+  pl->dtype = dtype;
+  pl->direction = direction;
+  pl->device = device;
+  pl->flags = flags;
+  pl->elem = dtype == EFFT_C64 ? 8 : 16;
+  cudaDeviceGetAttribute(&pl->num_sms, cudaDevAttrMultiProcessorCount, device);
+  int rc = build_plan(pl);
+  if (rc != EFFT_OK) {
+    delete pl;
+    return rc;
+  }
+  rc = finish_plan(pl);  // frees the plan itself on failure
+  if (rc != EFFT_OK) return rc;
+  *out = pl;
+  return EFFT_OK;
+}
+
+int efft_permute_swap01(const void* in, void* out, int64_t n0, int64_t n1, int64_t n2, int elem_bytes,
+                        void* stream) {
+  if (!in || !out || in == out) return fail(EFFT_ERR_INVALID_ARG, "bad buffers");
+  if (n0 < 1 || n1 < 1 || n2 < 1 || (elem_bytes != 8 && elem_bytes != 16))
+    return fail(EFFT_ERR_INVALID_ARG, "bad shape");
+  cudaStream_t s = (cudaStream_t)stream;
+  const int64_t words = n0 * n1 * n2 * elem_bytes / 16;
+  const unsigned grid = (unsigned)std::min<int64_t>((words + 255) / 256, 148 * 32);
+  if ((n2 * elem_bytes) % 16 == 0)
+    efft::swap01_kernel<uint4><<<grid, 256, 0, s>>>((const uint4*)in, (uint4*)out, n0, n1, n2 * elem_bytes / 16);
+  else
+    efft::swap01_kernel<uint2><<<grid, 256, 0, s>>>((const uint2*)in, (uint2*)out, n0, n1, n2);
+  CUDA_TRY(cudaGetLastError());
+  return EFFT_OK;
+}
+
+int efft_permute_swap12(const void* in, void* out, int64_t n0, int64_t n1, int64_t n2, int elem_bytes,
+                        void* stream) {
+  if (!in || !out || in == out) return fail(EFFT_ERR_INVALID_ARG, "bad buffers");
+  if (n0 < 1 || n1 < 1 || n2 < 1 || (elem_bytes != 8 && elem_bytes != 16) || n0 > 65535)
+    return fail(EFFT_ERR_INVALID_ARG, "bad shape");
+  cudaStream_t s = (cudaStream_t)stream;
+  dim3 grid((unsigned)((n2 + 31) / 32), (unsigned)((n1 + 31) / 32), (unsigned)n0), block(32, 8);
+  if (elem_bytes == 16)
+    efft::swap12_kernel<uint4><<<grid, block, 0, s>>>((const uint4*)in, (uint4*)out, n1, n2);
+  else
+    efft::swap12_kernel<uint2><<<grid, block, 0, s>>>((const uint2*)in, (uint2*)out, n1, n2);
+  CUDA_TRY(cudaGetLastError());
   return EFFT_OK;
 }
 
@@ -563,11 +677,12 @@ int efft_plan_launches(efft_plan_t pl, int* launches) {
 
 int efft_execute(efft_plan_t pl, const void* d_in, void* d_out, void* stream) {
   if (!pl || !d_in || !d_out) return fail(EFFT_ERR_INVALID_ARG, "NULL argument");
-  if (d_in == d_out) return fail(EFFT_ERR_INVALID_ARG, "in-place execution is not supported");
   const size_t bytes = (size_t)pl->n * pl->elem;
   const char* i0 = (const char*)d_in;
   const char* o0 = (const char*)d_out;
-  if (i0 < o0 + bytes && o0 < i0 + bytes) return fail(EFFT_ERR_INVALID_ARG, "input and output overlap");
+  // column plans are one position-preserving pass: in place is allowed
+  if (!(pl->columns && d_in == d_out) && i0 < o0 + bytes && o0 < i0 + bytes)
+    return fail(EFFT_ERR_INVALID_ARG, "input and output overlap");
   cudaStream_t s = (cudaStream_t)stream;
   CUDA_TRY(cudaSetDevice(pl->device));
   CUDA_TRY(cudaMemsetAsync(pl->counters, 0, pl->counter_bytes, s));

@@ -68,10 +68,61 @@ template <> struct VecT<double, 1> { using T = double2; };
 
 __device__ __forceinline__ float2 mk(float a, float b) { return make_float2(a, b); }
 __device__ __forceinline__ double2 mk(double a, double b) { return make_double2(a, b); }
+
+// ---- paired-fp32 (sm_100 FADD2 / FMUL2 / FFMA2) complex64 arithmetic: one
+// instruction per complex add, two per complex multiply; ptxas folds the
+// broadcast (x, x) / swapped (y, x) operand pairs into operand selectors.
+typedef unsigned long long u64;
+__device__ __forceinline__ u64 p64(float2 a) {
+  u64 d;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(d) : "f"(a.x), "f"(a.y));
+  return d;
+}
+__device__ __forceinline__ float2 f64p(u64 a) {
+  float2 r;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(r.x), "=f"(r.y) : "l"(a));
+  return r;
+}
+__device__ __forceinline__ float2 add2(float2 a, float2 b) {
+  u64 d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(p64(a)), "l"(p64(b)));
+  return f64p(d);
+}
+__device__ __forceinline__ float2 sub2(float2 a, float2 b) {
+  u64 d;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(p64(a)), "l"(p64(b)));
+  return f64p(d);
+}
+__device__ __forceinline__ float2 mul2(float2 a, float2 b) {
+  u64 d;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(p64(a)), "l"(p64(b)));
+  return f64p(d);
+}
+__device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c) {  // a*b + c per lane
+  u64 d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(p64(a)), "l"(p64(b)), "l"(p64(c)));
+  return f64p(d);
+}
+
 template <typename V> __device__ __forceinline__ V cadd(V a, V b) { return mk(a.x + b.x, a.y + b.y); }
 template <typename V> __device__ __forceinline__ V csub(V a, V b) { return mk(a.x - b.x, a.y - b.y); }
 template <typename V> __device__ __forceinline__ V cmul(V a, V b) {
   return mk(fma(a.x, b.x, -a.y * b.y), fma(a.x, b.y, a.y * b.x));
+}
+template <> __device__ __forceinline__ float2 cadd<float2>(float2 a, float2 b) { return add2(a, b); }
+template <> __device__ __forceinline__ float2 csub<float2>(float2 a, float2 b) { return sub2(a, b); }
+template <> __device__ __forceinline__ float2 cmul<float2>(float2 a, float2 b) {
+  // (a.x b.x - a.y b.y, a.x b.y + a.y b.x) = (a.x,a.x)*(b.x,b.y) + (a.y,a.y)*(-b.y,b.x)
+  return fma2(make_float2(a.y, a.y), make_float2(-b.y, b.x), mul2(make_float2(a.x, a.x), b));
+}
+// a + (-i) d and a - (-i) d (the radix-4 rotation fused into the add)
+__device__ __forceinline__ double2 add_mi(double2 a, double2 d) { return mk(a.x + d.y, a.y - d.x); }
+__device__ __forceinline__ double2 sub_mi(double2 a, double2 d) { return mk(a.x - d.y, a.y + d.x); }
+__device__ __forceinline__ float2 add_mi(float2 a, float2 d) {
+  return fma2(make_float2(d.y, d.x), make_float2(1.f, -1.f), a);
+}
+__device__ __forceinline__ float2 sub_mi(float2 a, float2 d) {
+  return fma2(make_float2(d.y, d.x), make_float2(-1.f, 1.f), a);
 }
 __device__ __forceinline__ float2 to_v(double2 w, float) { return make_float2((float)w.x, (float)w.y); }
 __device__ __forceinline__ double2 to_v(double2 w, double) { return w; }
@@ -219,21 +270,26 @@ __device__ __forceinline__ typename CT<R>::V twk(typename CT<R>::V b) {
     return mk(-b.x, -b.y);
   } else if constexpr (Q == 144) {
     return mk(-b.y, b.x);  // +i
-  } else if constexpr (Q == 24) {  // (1 - i)/sqrt2
+  } else if constexpr (Q == 24 || Q == 72 || Q == 120 || Q == 168) {
     constexpr R h = (R)0.70710678118654752440084436210484903928;
-    return mk((b.x + b.y) * h, (b.y - b.x) * h);
-  } else if constexpr (Q == 72) {  // (-1 - i)/sqrt2
-    constexpr R h = (R)0.70710678118654752440084436210484903928;
-    return mk((b.y - b.x) * h, -(b.x + b.y) * h);
-  } else if constexpr (Q == 120) {  // (-1 + i)/sqrt2
-    constexpr R h = (R)0.70710678118654752440084436210484903928;
-    return mk(-(b.x + b.y) * h, (b.x - b.y) * h);
-  } else if constexpr (Q == 168) {  // (1 + i)/sqrt2
-    constexpr R h = (R)0.70710678118654752440084436210484903928;
-    return mk((b.x - b.y) * h, (b.x + b.y) * h);
+    if constexpr (sizeof(R) == 4) {
+      // h*(b + (-i)b) etc: one FFMA2 for the rotation-add, one FMUL2 for the scale
+      if constexpr (Q == 24) return mul2(add_mi(b, b), make_float2(h, h));   // (1 - i)/sqrt2
+      if constexpr (Q == 72) return mul2(sub_mi(b, b), make_float2(-h, -h));  // (-1 - i)/sqrt2
+      if constexpr (Q == 120) return mul2(add_mi(b, b), make_float2(-h, -h));  // (-1 + i)/sqrt2 = -(1 - i)/sqrt2
+      if constexpr (Q == 168) return mul2(sub_mi(b, b), make_float2(h, h));   // (1 + i)/sqrt2
+    } else {
+      if constexpr (Q == 24) return mk((b.x + b.y) * h, (b.y - b.x) * h);
+      if constexpr (Q == 72) return mk((b.y - b.x) * h, -(b.x + b.y) * h);
+      if constexpr (Q == 120) return mk(-(b.x + b.y) * h, (b.x - b.y) * h);
+      if constexpr (Q == 168) return mk((b.x - b.y) * h, (b.x + b.y) * h);
+    }
   } else {
     constexpr R wr = (R)W192::v[Q][0], wi = (R)W192::v[Q][1];
-    return mk(fma(b.x, wr, -b.y * wi), fma(b.x, wi, b.y * wr));
+    if constexpr (sizeof(R) == 4)
+      return fma2(make_float2(b.y, b.y), make_float2(-wi, wr), mul2(make_float2(b.x, b.x), make_float2(wr, wi)));
+    else
+      return mk(fma(b.x, wr, -b.y * wi), fma(b.x, wi, b.y * wr));
   }
 }
 
@@ -248,11 +304,10 @@ template <typename V> __device__ __forceinline__ void dft2(V* a) {
 template <typename V> __device__ __forceinline__ void dft4(V* a) {
   V t0 = cadd(a[0], a[2]), t1 = csub(a[0], a[2]);
   V t2 = cadd(a[1], a[3]), d = csub(a[1], a[3]);
-  V t3 = mk(d.y, -d.x);  // (a1 - a3) * (-i)
   a[0] = cadd(t0, t2);
-  a[1] = cadd(t1, t3);
+  a[1] = add_mi(t1, d);  // t1 + (a1 - a3)(-i)
   a[2] = csub(t0, t2);
-  a[3] = csub(t1, t3);
+  a[3] = sub_mi(t1, d);
 }
 template <typename V> __device__ __forceinline__ void dft3(V* a) {
   using R = decltype(a[0].x);
@@ -319,7 +374,7 @@ struct SubDesc {
   int64_t ig, it, is, im;  // load offsets (elements); columns are unit stride
   int64_t og, ot, of, os, om;  // store offsets (elements)
   int64_t tw_mod;          // modulus of the fused DIT twiddle, 0 = none
-  int64_t Ag, At, Af, As;  // A = grp*Ag + task*At + f*Af + s*As
+  int64_t A0, Ag, At, Af, As;  // A = A0 + grp*Ag + task*At + f*Af + s*As
   int64_t C0, Ct, Cs, Cm;  // C = C0 + task*Ct + s*Cs + m*Cm ; e = A*C mod tw_mod
   int32_t ntasks;          // tasks per column group
   int32_t in_staging, out_staging;
@@ -632,7 +687,7 @@ struct Tile {
       coords<S0>(q, fv, u, s);
       const int64_t C = d.C0 + task * d.Ct + s * d.Cs + (int64_t)u * d.Cm;
       if (VEC > 1 && d.Af == 0) {  // one twiddle series serves all VEC columns
-        const int64_t A = grp * d.Ag + task * d.At + s * d.As;
+        const int64_t A = d.A0 + grp * d.Ag + task * d.At + s * d.As;
         double2 w = wroot(mulmod(A, C, M), M);
         const double2 st = wroot(mulmod(A, d.Cm * L0, M), M);
 #pragma unroll
@@ -646,7 +701,7 @@ struct Tile {
       }
 #pragma unroll
       for (int c = 0; c < VEC; ++c) {
-        const int64_t A = grp * d.Ag + task * d.At + (fv * VEC + c) * d.Af + s * d.As;
+        const int64_t A = d.A0 + grp * d.Ag + task * d.At + (fv * VEC + c) * d.Af + s * d.As;
         double2 w = wroot(mulmod(A, C, M), M);
         const double2 st = wroot(mulmod(A, d.Cm * L0, M), M);
         V* vv = v + (q * VEC + c) * S0;
@@ -797,12 +852,14 @@ struct Tile {
     }
   }
 
-  // One tile: load (+conj, +finite check, +DIT twiddle), RHO-point DFTs, store.
-  __device__ static void run(const SubDesc& d, const PassArgs& p, int64_t grp, int task, int slot, V* sm,
-                             const V* tw, bool& nonfinite, int32_t* release = nullptr) {
-    V v[E];
-    const V* src = d.in_staging ? (const V*)p.staging + slot * p.slot_elems + task * d.it
-                                : (const V*)p.in + grp * d.ig + task * d.it;
+  __device__ __forceinline__ static const V* source(const SubDesc& d, const PassArgs& p, int64_t grp, int task,
+                                                     int slot) {
+    return d.in_staging ? (const V*)p.staging + (int64_t)slot * p.slot_elems + task * d.it
+                        : (const V*)p.in + grp * d.ig + task * d.it;
+  }
+
+  __device__ __forceinline__ static void load_any(const SubDesc& d, const V* src, int64_t grp, V* v,
+                                                  bool& nonfinite) {
     if (d.conj_in) {
       if (d.check_finite)
         load<true, true>(d, src, grp, v, nonfinite);
@@ -813,9 +870,15 @@ struct Tile {
     } else {
       load<false, false>(d, src, grp, v, nonfinite);
     }
+  }
+
+  // Everything after the load: DIT twiddle, radix stages, store.  For a tile
+  // that read the staging ring (`release` set), the consumed rows are
+  // discarded and the slot released once stage 0 has consumed the registers.
+  __device__ __forceinline__ static void process(const SubDesc& d, const PassArgs& p, int64_t grp, int task,
+                                                 int slot, V* v, V* sm, const V* tw, int32_t* release,
+                                                 const V* src) {
     if (d.tw_mod) twiddle(d, grp, task, v);
-    // in-CTA radix stages; stage 0 consumes the loaded registers, after which the
-    // staging slot this tile read can be released to its producers
     if (release != nullptr) {
       stage_compute<0>(v, tw);
       discard_loaded(d, src);
@@ -833,6 +896,15 @@ struct Tile {
       stages<0>(v, sm, tw);
     }
     store(d, p, grp, task, slot, v, sm);
+  }
+
+  // One tile: load (+conj, +finite check, +DIT twiddle), RHO-point DFTs, store.
+  __device__ static void run(const SubDesc& d, const PassArgs& p, int64_t grp, int task, int slot, V* sm,
+                             const V* tw, bool& nonfinite, int32_t* release = nullptr) {
+    V v[E];
+    const V* src = source(d, p, grp, task, slot);
+    load_any(d, src, grp, v, nonfinite);
+    process(d, p, grp, task, slot, v, sm, tw, release, src);
   }
 
   __device__ __forceinline__ static void fixup(const SubDesc& d, V* v, bool& nonfinite) {
@@ -920,7 +992,9 @@ __device__ __forceinline__ void decode_task(const PassArgs& p, int64_t pos, bool
 // order (A(0..lag-1), then B(g-lag), A(g) pairs, then the tail of B), which
 // makes every wait target a task that an already-running CTA owns.
 // occupancy target: small (32 KB) tiles run 4 CTAs per SM, 64 KB tiles 2
-template <class TA> constexpr int min_blocks() { return TA::NT >= 512 ? 1 : (TA::TILE <= 4096 ? 4 : 2); }
+template <class TA> constexpr int min_blocks() {
+  return TA::NT >= 512 ? 1 : (TA::TILE * (int)sizeof(typename TA::V) <= 32768 ? 4 : 2);
+}
 
 template <typename R, class TA, class TB>
 __global__ void __launch_bounds__(TA::NT, min_blocks<TA>()) pass_kernel(const __grid_constant__ PassArgs p) {
@@ -999,8 +1073,8 @@ __global__ void __launch_bounds__(TA::NT, min_blocks<TA>()) pass_kernel(const __
 //     (registers + the same buffer for exchanges, named barrier 1), store,
 //     then release the buffer (empty mbarrier) and, for A tasks, publish the
 //     group counter.
-template <typename R, class TA, class TB>
-__global__ void __launch_bounds__(TA::NT + 32, 1) staged_kernel(const __grid_constant__ PassArgs p) {  // NOLINT
+template <typename R, class TA, class TB, int NBUF = 2>
+__global__ void __launch_bounds__(TA::NT + 32, 1) staged_kernel(const __grid_constant__ PassArgs p) {
   using V = typename CT<R>::V;
   static_assert(TA::NT == TB::NT && TA::TOFF == 32 && TB::TOFF == 32, "consumer warps follow warp 0");
   static_assert(TA::SWZ && TB::SWZ, "TMA tiles land 128B-swizzled");
@@ -1009,16 +1083,16 @@ __global__ void __launch_bounds__(TA::NT + 32, 1) staged_kernel(const __grid_con
   static_assert((BUF * sizeof(V)) % 1024 == 0, "swizzled buffers stay 1024-byte aligned");
   // 128B swizzle needs 1024-byte aligned buffers (the launch adds 1 KB slack)
   V* bufs = reinterpret_cast<V*>(smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u));
-  V* twA = bufs + 2 * BUF;
+  V* twA = bufs + NBUF * BUF;
   V* twB = twA + TA::RHO;
-  __shared__ __align__(8) uint64_t full[2], empty[2];
-  __shared__ long long task_of[2], task_grp[2];
-  __shared__ int task_sub[2], task_slot[2], task_isB[2];
+  __shared__ __align__(8) uint64_t full[NBUF], empty[NBUF];
+  __shared__ long long task_of[NBUF], task_grp[NBUF];
+  __shared__ int task_sub[NBUF], task_slot[NBUF], task_isB[NBUF];
   if (threadIdx.x == 0) {
-    mbar_init(&full[0], 1);
-    mbar_init(&full[1], 1);
-    mbar_init(&empty[0], TA::NT / 32);
-    mbar_init(&empty[1], TA::NT / 32);
+    for (int i = 0; i < NBUF; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], TA::NT / 32);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   TA::build_table(twA);
@@ -1028,8 +1102,8 @@ __global__ void __launch_bounds__(TA::NT + 32, 1) staged_kernel(const __grid_con
   if (warp == 0) {
     const uint64_t pol = policy_evict_first();
     for (int64_t k = 0;; ++k) {
-      const int b = (int)(k & 1);
-      if (k >= 2) mbar_wait(&empty[b], (uint32_t)(((k >> 1) - 1) & 1));
+      const int b = (int)(k % NBUF);
+      if (k >= NBUF) mbar_wait(&empty[b], (uint32_t)(((k / NBUF) - 1) & 1));
       unsigned long long pos = 0;
       if (lane == 0) pos = atomicAdd(p.task_counter, 1ull);
       pos = __shfl_sync(0xffffffffu, pos, 0);
@@ -1082,8 +1156,8 @@ __global__ void __launch_bounds__(TA::NT + 32, 1) staged_kernel(const __grid_con
   } else {
     bool nonfinite = false;
     for (int64_t k = 0;; ++k) {
-      const int b = (int)(k & 1);
-      mbar_wait(&full[b], (uint32_t)((k >> 1) & 1));
+      const int b = (int)(k % NBUF);
+      mbar_wait(&full[b], (uint32_t)((k / NBUF) & 1));
       const long long pos = task_of[b];
       if (pos < 0) break;
       const bool isB = task_isB[b];
@@ -1107,6 +1181,272 @@ __global__ void __launch_bounds__(TA::NT + 32, 1) staged_kernel(const __grid_con
       }
     }
     if (nonfinite) atomicOr(p.flag, 1);
+  }
+}
+
+// Software-pipelined persistent staged pass (register double buffering).
+// Each CTA claims task k+1 while it works on task k and, if k+1's dependency
+// is already satisfied (non-blocking check), issues k+1's global loads into a
+// second register set BEFORE computing task k, so the DRAM / L2 latency of the
+// next tile hides behind the current tile's DFT work.  If the dependency is
+// not ready yet the load is deferred until task k is done (a blocking wait is
+// then deadlock-free: every wait targets an earlier task and this CTA holds
+// no unfinished task).
+template <typename R, class TA, class TB>
+__global__ void __launch_bounds__(TA::NT, 1) pf_kernel(const __grid_constant__ PassArgs p) {
+  using V = typename CT<R>::V;
+  static_assert(TA::E == TB::E && TA::NT == TB::NT, "A and B tiles share the register footprint");
+  constexpr int E = TA::E;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  constexpr int SM_ELEMS = TA::SMEM_ELEMS > TB::SMEM_ELEMS ? TA::SMEM_ELEMS : TB::SMEM_ELEMS;
+  V* sm = reinterpret_cast<V*>(smem_raw);
+  V* twA = sm + SM_ELEMS;
+  V* twB = twA + TA::RHO;
+  __shared__ long long s_pos[2], s_grp[2];
+  __shared__ int s_sub[2], s_slot[2], s_isB[2], s_ready[2];
+  TA::build_table(twA);
+  TB::build_table(twB);
+  const int64_t G = p.ngroups;
+  (void)G;
+  auto publish = [&](int b, unsigned long long pos) {  // thread 0
+    s_pos[b] = (long long)pos;
+    if ((int64_t)pos >= p.total_tasks) return;
+    bool isB;
+    int64_t grp, sub;
+    decode_task(p, (int64_t)pos, isB, grp, sub);
+    s_isB[b] = isB;
+    s_grp[b] = grp;
+    s_sub[b] = (int)sub;
+    s_slot[b] = (int)(grp % p.nslots);
+    const int32_t* ctr = isB ? p.doneA + grp : (grp >= p.nslots ? p.doneB + (grp - p.nslots) : nullptr);
+    const int32_t need = isB ? p.a.ntasks : p.b.ntasks;
+    const bool ok = ctr == nullptr || *(volatile const int32_t*)ctr >= need;
+    if (ok) __threadfence();
+    s_ready[b] = ok;
+  };
+  auto wait_dep = [&](int b) {  // all threads; blocking
+    if (threadIdx.x == 0) {
+      const int64_t grp = s_grp[b];
+      const bool isB = s_isB[b];
+      const int32_t* ctr = isB ? p.doneA + grp : (grp >= p.nslots ? p.doneB + (grp - p.nslots) : nullptr);
+      const int32_t need = isB ? p.a.ntasks : p.b.ntasks;
+      if (ctr != nullptr) {
+        while (*(volatile const int32_t*)ctr < need) __nanosleep(64);
+        __threadfence();
+      }
+    }
+    __syncthreads();
+  };
+  auto load_task = [&](int b, V* v, bool& nf) {
+    const int64_t grp = s_grp[b];
+    const int sub = s_sub[b], slot = s_slot[b];
+    if (s_isB[b])
+      TB::load_any(p.b, TB::source(p.b, p, grp, sub, slot), grp, v, nf);
+    else
+      TA::load_any(p.a, TA::source(p.a, p, grp, sub, slot), grp, v, nf);
+  };
+  bool nonfinite = false;
+  V cur[E], nxt[E];
+  if (threadIdx.x == 0) publish(0, atomicAdd(p.task_counter, 1ull));
+  __syncthreads();
+  if (s_pos[0] >= p.total_tasks) return;
+  wait_dep(0);
+  load_task(0, cur, nonfinite);
+  int b = 0;
+  for (;;) {
+    // claim and decode the next task; prefetch its tile if its producers are done
+    if (threadIdx.x == 0) publish(b ^ 1, atomicAdd(p.task_counter, 1ull));
+    __syncthreads();
+    const bool has_next = s_pos[b ^ 1] < p.total_tasks;
+    const bool early = has_next && s_ready[b ^ 1];
+    if (early) load_task(b ^ 1, nxt, nonfinite);
+    // process the current task
+    {
+      const int64_t grp = s_grp[b];
+      const int sub = s_sub[b], slot = s_slot[b];
+      if (!s_isB[b]) {
+        TA::process(p.a, p, grp, sub, slot, cur, sm, twA, nullptr, nullptr);
+        __syncthreads();
+        if (threadIdx.x == 0) {
+          __threadfence();
+          atomicAdd(p.doneA + grp, 1);
+        }
+      } else {
+        TB::process(p.b, p, grp, sub, slot, cur, sm, twB, p.doneB + grp, TB::source(p.b, p, grp, sub, slot));
+      }
+      __syncthreads();
+    }
+    if (!has_next) break;
+    if (!early) {
+      wait_dep(b ^ 1);
+      load_task(b ^ 1, nxt, nonfinite);
+    }
+#pragma unroll
+    for (int i = 0; i < E; ++i) cur[i] = nxt[i];
+    b ^= 1;
+  }
+  if (__syncthreads_or(nonfinite) && threadIdx.x == 0) atomicOr(p.flag, 1);
+}
+
+// TMA-prefetching persistent staged pass (no dedicated producer warp).
+// Thread 0 keeps the next NBUF-1 tiles in flight: between tasks it claims a
+// task, checks its dependency without blocking, and issues one TMA tensor
+// copy of the tile (128B-swizzled) into a free shared-memory buffer,
+// completing that buffer's mbarrier.  All NT threads compute the current tile
+// from its buffer (which then doubles as the exchange buffer).  A tile whose
+// producers were not finished when it was claimed is copied later, just
+// before it is needed; that blocking wait is deadlock-free because by then
+// every earlier task held by this CTA is complete.
+template <typename R, class TA, class TB, int NBUF>
+__global__ void __launch_bounds__(TA::NT, 1) tp_kernel(const __grid_constant__ PassArgs p) {
+  using V = typename CT<R>::V;
+  static_assert(TA::NT == TB::NT && TA::TOFF == 0 && TB::TOFF == 0, "all threads compute");
+  static_assert(TA::SWZ && TB::SWZ, "TMA tiles land 128B-swizzled");
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  constexpr int BUF = TA::SMEM_ELEMS > TB::SMEM_ELEMS ? TA::SMEM_ELEMS : TB::SMEM_ELEMS;
+  static_assert((BUF * sizeof(V)) % 1024 == 0, "swizzled buffers stay 1024-byte aligned");
+  V* bufs = reinterpret_cast<V*>(smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u));
+  V* twA = bufs + NBUF * BUF;
+  V* twB = twA + TA::RHO;
+  __shared__ __align__(8) uint64_t full[NBUF];
+  __shared__ long long t_pos[NBUF], t_grp[NBUF];
+  __shared__ int t_sub[NBUF], t_slot[NBUF], t_isB[NBUF], t_issued[NBUF], t_phase[NBUF];
+  if (threadIdx.x == 0)
+    for (int i = 0; i < NBUF; ++i) {
+      mbar_init(&full[i], 1);
+      t_phase[i] = 0;
+    }
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  TA::build_table(twA);
+  TB::build_table(twB);
+  const uint64_t pol = policy_evict_first();
+  // ---- thread-0 helpers
+  auto dep_ok = [&](int b, bool block) -> bool {
+    const int64_t grp = t_grp[b];
+    const bool isB = t_isB[b];
+    const int32_t* ctr = isB ? p.doneA + grp : (grp >= p.nslots ? p.doneB + (grp - p.nslots) : nullptr);
+    if (ctr == nullptr) return true;
+    const int32_t need = isB ? p.a.ntasks : p.b.ntasks;
+    if (block) {
+      while (*(volatile const int32_t*)ctr < need) __nanosleep(64);
+    } else if (*(volatile const int32_t*)ctr < need) {
+      return false;
+    }
+    __threadfence();
+    fence_proxy_async();
+    return true;
+  };
+  auto issue = [&](int b) {
+    V* dst = bufs + b * BUF;
+    const int64_t grp = t_grp[b];
+    const int sub = t_sub[b];
+    if (!t_isB[b]) {
+      constexpr int W = (int)sizeof(V) / 8;
+      constexpr int BOX = TA::RHO > 256 ? TA::RHO / 2 : TA::RHO;
+      mbar_arrive_tx(&full[b], (uint32_t)(TA::D * TA::RHO * 128));
+#pragma unroll
+      for (int h = 0; h < TA::RHO / BOX; ++h)
+        tma_load_3d(dst + h * BOX * TA::D * TA::F, &p.tmA, (int)(grp * TA::F * W), sub * TA::D, h * BOX,
+                    &full[b], pol);
+    } else {
+      constexpr int BOX = TB::RHO > 256 ? TB::RHO / 2 : TB::RHO;
+      mbar_arrive_tx(&full[b], (uint32_t)(TB::D * TB::RHO * 128));
+#pragma unroll
+      for (int h = 0; h < TB::RHO / BOX; ++h)
+        tma_load_4d(dst + h * BOX * TB::D * TB::F, &p.tmB, 0, sub * TB::D, h * BOX, t_slot[b], &full[b], pol);
+    }
+    t_issued[b] = 1;
+  };
+  // task positions are fetched one claim ahead so the atomic's round trip
+  // hides behind a tile's compute instead of stalling the whole CTA
+  unsigned long long next_pos = 0;
+  auto claim = [&](int b) {  // claim a task into buffer b; issue its copy if its producers are done
+    const unsigned long long pos = next_pos;
+    next_pos = atomicAdd(p.task_counter, 1ull);
+    t_pos[b] = (long long)pos;
+    t_issued[b] = 0;
+    if ((int64_t)pos >= p.total_tasks) return;
+    bool isB;
+    int64_t grp, sub;
+    decode_task(p, (int64_t)pos, isB, grp, sub);
+    t_isB[b] = isB;
+    t_grp[b] = grp;
+    t_sub[b] = (int)sub;
+    t_slot[b] = (int)(grp % p.nslots);
+    if (dep_ok(b, false)) issue(b);
+  };
+  if (threadIdx.x == 0) {
+    next_pos = atomicAdd(p.task_counter, 1ull);
+    for (int i = 0; i < NBUF - 1; ++i) claim(i);
+  }
+  __syncthreads();
+  bool nonfinite = false;
+  for (int64_t k = 0;; ++k) {
+    const int b = (int)(k % NBUF);
+    if (threadIdx.x == 0) {
+      // refill the buffer freed by task k-1 with the next claim, and make sure
+      // task k's own copy is under way (blocking on its producers if needed)
+      claim((int)((k + NBUF - 1) % NBUF));
+      if (t_pos[b] < p.total_tasks && !t_issued[b]) {
+        dep_ok(b, true);
+        issue(b);
+      }
+    }
+    __syncthreads();
+    if (t_pos[b] >= p.total_tasks) break;
+    mbar_wait(&full[b], (uint32_t)t_phase[b]);
+    const bool isB = t_isB[b];
+    const int64_t grp = t_grp[b];
+    const int sub = t_sub[b], slot = t_slot[b];
+    V* buf = bufs + b * BUF;
+    if (!isB) {
+      TA::run_smem(p.a, p, grp, sub, slot, buf, twA, nonfinite, nullptr, nullptr);
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        __threadfence();
+        atomicAdd(p.doneA + grp, 1);
+      }
+    } else {
+      const V* stg = (const V*)p.staging + (int64_t)slot * p.slot_elems + (int64_t)sub * p.b.it;
+      TB::run_smem(p.b, p, grp, sub, slot, buf, twB, nonfinite, p.doneB + grp, stg);
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) t_phase[b] ^= 1;
+  }
+  if (__syncthreads_or(nonfinite) && threadIdx.x == 0) atomicOr(p.flag, 1);
+}
+
+// ----------------------------------------------------------------------------
+// Block permutations used by the sharded (multi-GPU) six-step: pack/unpack of
+// all-to-all chunks.  Elements are opaque 8- or 16-byte words (VT).
+// ----------------------------------------------------------------------------
+// out[b][a][c] = in[a][b][c], shapes (n0, n1, n2): the two outer dims swap, the
+// contiguous inner dim is copied with 16-byte vectors.
+template <typename W>
+__global__ void swap01_kernel(const W* __restrict__ in, W* __restrict__ out, int64_t n0, int64_t n1, int64_t n2) {
+  const int64_t total = n0 * n1 * n2;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t c = i % n2, ab = i / n2, b = ab % n1, a = ab / n1;
+    out[(b * n0 + a) * n2 + c] = in[i];
+  }
+}
+// out[a][c][b] = in[a][b][c], shapes (n0, n1, n2): a batched 2D transpose
+// through a padded 32x33 shared-memory tile.
+template <typename W>
+__global__ void swap12_kernel(const W* __restrict__ in, W* __restrict__ out, int64_t n1, int64_t n2) {
+  __shared__ W t[32][33];
+  const int64_t a = blockIdx.z;
+  const int64_t b0 = blockIdx.y * 32, c0 = blockIdx.x * 32;
+  const W* src = in + a * n1 * n2;
+  W* dst = out + a * n1 * n2;
+  for (int y = threadIdx.y; y < 32; y += blockDim.y) {
+    const int64_t b = b0 + y, c = c0 + threadIdx.x;
+    if (b < n1 && c < n2) t[y][threadIdx.x] = src[b * n2 + c];
+  }
+  __syncthreads();
+  for (int y = threadIdx.y; y < 32; y += blockDim.y) {
+    const int64_t c = c0 + y, b = b0 + threadIdx.x;
+    if (b < n1 && c < n2) dst[c * n1 + b] = t[threadIdx.x][y];
   }
 }
 

@@ -15,9 +15,9 @@ bool get_direct_kernel_f32(int rho, KernelInfo* out) {
 #undef D2
 #undef D3
 
-// complex64 warp-specialised tiles: 16 consumer warps, 16 elements per thread
-template <int RHO> using ST16 = Tile<float, RHO, (RHO % 3 ? 512 : 384) / RHO, 512, false, 1, 32, 1, true>;
-#define SA(rb) case rb: *out = make_info<float, ST16<RA>, ST16<rb>, true>(); return true;
+// complex64 warp-specialised tiles: 8 consumer warps x 32 elements (radix-32
+// stages), three TMA buffers in flight
+#define SA(rb) case rb: *out = make_info<float, ST<float, RA>, ST<float, rb>, true, false, 3>(); return true;
 template <int RA>
 static bool staged_f32(int rho_b, KernelInfo* out) {
   switch (rho_b) {
@@ -42,6 +42,37 @@ static bool staged_reg_f32(int rho_b, KernelInfo* out) {
 // radix-16 stages, 4 CTAs (32 warps) per SM
 template <int RHO> using SM32 = Tile<float, RHO, 256 / RHO, 256, false, 1>;
 #define SS(rb) case rb: *out = make_info<float, SM32<256>, SM32<rb>>(); return true;
+// 64 KB complex64 tiles with 512 threads (16 elements each, 2 CTAs = 32 warps per SM)
+template <int RHO> using W512 = Tile<float, RHO, 512 / RHO, 512, false, 1>;
+#define SW(rb) case rb: *out = make_info<float, W512<256>, W512<rb>>(); return true;
+#define SP(rb) case rb: *out = make_info<float, W512<256>, W512<rb>, false, true>(); return true;
+// software-pipelined (register double-buffered) variant of the same tiles
+bool get_staged_pf_f32(int rho_b, KernelInfo* out) {
+  switch (rho_b) {
+    SP(8) SP(16) SP(32) SP(64) SP(128) SP(256)
+    default: return false;
+  }
+}
+#undef SP
+bool get_staged_wide_f32(int rho_b, KernelInfo* out) {
+  switch (rho_b) {
+    SW(8) SW(16) SW(32) SW(64) SW(128) SW(256)
+    default: return false;
+  }
+}
+#undef SW
+
+// TMA-prefetching tiles: 512 threads x 16 elements, 3 buffers in flight
+template <int RHO> using TP16 = Tile<float, RHO, 512 / RHO, 512, false, 1, 0, 0, true>;
+#define ST3(rb) case rb: *out = make_info<float, TP16<256>, TP16<rb>, false, false, 3, true>(); return true;
+bool get_staged_tp_f32(int rho_b, KernelInfo* out) {
+  switch (rho_b) {
+    ST3(8) ST3(16) ST3(32) ST3(64) ST3(128) ST3(256)
+    default: return false;
+  }
+}
+#undef ST3
+
 bool get_staged_small_f32(int rho_b, KernelInfo* out) {
   switch (rho_b) {
     SS(2) SS(4) SS(8) SS(16) SS(32) SS(64) SS(128) SS(256)
