@@ -153,7 +153,7 @@ bool get_staged(int dtype, int ra, int rb, KernelInfo* k) {
 
 
 // Decide direct vs staged and the sub-radices of one pass of radix R.
-bool pick_pass(int dtype, int64_t R, PassPlan* pp) {
+bool pick_pass(int dtype, int64_t R, PassPlan* pp, int64_t ncols = 0) {
   pp->radix = R;
   const bool has3 = (R % 3) == 0;
   const int64_t dmax = has3 ? 384 : 512;
@@ -161,6 +161,11 @@ bool pick_pass(int dtype, int64_t R, PassPlan* pp) {
     pp->staged = false;
     pp->rho_a = R;
     pp->rho_b = 0;
+    // TMA-prefetching direct tiles when every tile is full (EFFT_DIRECT_TP=1)
+    static const int dtp = env_int("EFFT_DIRECT_TP", 0);
+    if (dtp && dtype == EFFT_C64 && !has3 && R >= 16 && ncols > 0 && efft::get_direct_tp_f32((int)R, &pp->k) &&
+        ncols % (pp->k.d_a * 16) == 0)
+      return true;
     return get_direct(dtype, (int)R, &pp->k);
   }
   pp->staged = true;
@@ -175,6 +180,8 @@ bool pick_pass(int dtype, int64_t R, PassPlan* pp) {
     ok = efft::get_staged_small_f32((int)pp->rho_b, &pp->k);
   else if (dtype == EFFT_C64 && !has3 && c64_tile == 1 && !ws && pp->rho_b >= 8 && pp->rho_b <= 256)
     ok = efft::get_staged_wide_f32((int)pp->rho_b, &pp->k);
+  else if (dtype == EFFT_C64 && !has3 && c64_tile == 4 && pp->rho_b >= 8 && pp->rho_b <= 256)
+    ok = efft::get_staged_ws32_f32((int)pp->rho_b, &pp->k);
   else if (!has3 && c64_tile == 3 && !ws && pp->rho_b >= 8 && pp->rho_b <= 256)
     ok = dtype == EFFT_C64 ? efft::get_staged_tp_f32((int)pp->rho_b, &pp->k)
                            : efft::get_staged_tp_f64((int)pp->rho_b, &pp->k);
@@ -346,6 +353,24 @@ int encode_A(efft_plan_s* pl, PassPlan& pp, const void* base) {
   return EFFT_OK;
 }
 
+// TMA map of a direct pass's tiles over its input: [f (uint64 units), column group, row]
+int encode_D(efft_plan_s* pl, PassPlan& pp, const void* base) {
+  EncodeTiledFn enc = encode_fn();
+  if (!enc) return fail(EFFT_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  const int64_t N = pl->n, R = pp.radix, C = N / R, w = (int64_t)pl->elem / 8;
+  const int F = 128 / (int)pl->elem;
+  cuuint64_t dims[3] = {(cuuint64_t)(F * w), (cuuint64_t)(C / F), (cuuint64_t)R};
+  cuuint64_t strides[2] = {(cuuint64_t)(F * pl->elem), (cuuint64_t)(C * pl->elem)};
+  cuuint32_t box[3] = {(cuuint32_t)(F * w), (cuuint32_t)pp.k.d_a, (cuuint32_t)(R > 256 ? R / 2 : R)};
+  cuuint32_t es[3] = {1, 1, 1};
+  CUresult r = enc(&pp.args.tmA, CU_TENSOR_MAP_DATA_TYPE_UINT64, 3, const_cast<void*>(base), dims, strides, box, es,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(EFFT_ERR_CUDA, "tensor map (direct) encode failed: %d", (int)r);
+  pp.tmA_ptr = base;
+  return EFFT_OK;
+}
+
 // TMA map of a staged pass's B tiles over the staging ring: [f, k1, u, slot]
 int encode_B(efft_plan_s* pl, PassPlan& pp) {
   EncodeTiledFn enc = encode_fn();
@@ -424,7 +449,7 @@ int build_plan(efft_plan_s* pl) {
   size_t staging_bytes = 0;
   for (int p = 0; p < pl->npass; ++p) {
     PassPlan& pp = pl->pass[p];
-    if (!pick_pass(dt, radices[p], &pp))
+    if (!pick_pass(dt, radices[p], &pp, pl->n / radices[p]))
       return fail(EFFT_ERR_UNSUPPORTED_SIZE, "no kernel for radix %lld", (long long)radices[p]);
     describe_pass(pl, p, pl->npass, radices[p], pl->columns ? pl->col_count : ns);
     if (pl->columns) {  // column store (Ns = cols), caller-chosen twiddle, unscaled inverse
@@ -690,8 +715,8 @@ int efft_execute(efft_plan_t pl, const void* d_in, void* d_out, void* stream) {
     if (pl->timing) CUDA_TRY(cudaEventRecord(pl->ev[p], s));
     PassPlan& pp = pl->pass[p];
     const void* src = p == 0 ? d_in : d_out;
-    if (pp.staged && pp.k.ws && pp.tmA_ptr != src) {
-      int rc = encode_A(pl, pp, src);
+    if (pp.k.ws && pp.tmA_ptr != src) {
+      int rc = pp.staged ? encode_A(pl, pp, src) : encode_D(pl, pp, src);
       if (rc != EFFT_OK) return rc;
     }
     PassArgs a = pp.args;

@@ -1074,7 +1074,8 @@ __global__ void __launch_bounds__(TA::NT, min_blocks<TA>()) pass_kernel(const __
 //     then release the buffer (empty mbarrier) and, for A tasks, publish the
 //     group counter.
 template <typename R, class TA, class TB, int NBUF = 2>
-__global__ void __launch_bounds__(TA::NT + 32, 1) staged_kernel(const __grid_constant__ PassArgs p) {
+__global__ void __launch_bounds__(TA::NT + 32, (TA::TILE * (int)sizeof(typename TA::V) <= 32768 ? 2 : 1))
+    staged_kernel(const __grid_constant__ PassArgs p) {
   using V = typename CT<R>::V;
   static_assert(TA::NT == TB::NT && TA::TOFF == 32 && TB::TOFF == 32, "consumer warps follow warp 0");
   static_assert(TA::SWZ && TB::SWZ, "TMA tiles land 128B-swizzled");
@@ -1412,6 +1413,52 @@ __global__ void __launch_bounds__(TA::NT, 1) tp_kernel(const __grid_constant__ P
       __syncthreads();
     }
     if (threadIdx.x == 0) t_phase[b] ^= 1;
+  }
+  if (__syncthreads_or(nonfinite) && threadIdx.x == 0) atomicOr(p.flag, 1);
+}
+
+// TMA-prefetching DIRECT pass (one tile type, no staging, no dependencies):
+// static round-robin schedule (task = blockIdx + k*gridDim), thread 0 keeps
+// NBUF-1 tiles in flight with one TMA tensor copy each, all threads compute.
+template <typename R, class TA, int NBUF>
+__global__ void __launch_bounds__(TA::NT, 1) tpd_kernel(const __grid_constant__ PassArgs p) {
+  using V = typename CT<R>::V;
+  static_assert(TA::SWZ && TA::TOFF == 0, "TMA tiles, all threads compute");
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  constexpr int BUF = TA::SMEM_ELEMS;
+  static_assert((BUF * sizeof(V)) % 1024 == 0, "swizzled buffers stay 1024-byte aligned");
+  V* bufs = reinterpret_cast<V*>(smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u));
+  V* tw = bufs + NBUF * BUF;
+  __shared__ __align__(8) uint64_t full[NBUF];
+  if (threadIdx.x == 0)
+    for (int i = 0; i < NBUF; ++i) mbar_init(&full[i], 1);
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  TA::build_table(tw);
+  const uint64_t pol = policy_evict_first();
+  const int64_t T = p.total_tasks;
+  auto issue = [&](int64_t task, int b) {
+    if (task >= T) return;
+    V* dst = bufs + b * BUF;
+    constexpr int BOX = TA::RHO > 256 ? TA::RHO / 2 : TA::RHO;
+    mbar_arrive_tx(&full[b], (uint32_t)(TA::D * TA::RHO * 128));
+#pragma unroll
+    for (int h = 0; h < TA::RHO / BOX; ++h)
+      tma_load_3d(dst + h * BOX * TA::D * TA::F, &p.tmA, 0, (int)(task * TA::D), h * BOX, &full[b], pol);
+  };
+  if (threadIdx.x == 0)
+    for (int i = 0; i < NBUF - 1; ++i) issue(blockIdx.x + (int64_t)i * gridDim.x, i);
+  __syncthreads();
+  bool nonfinite = false;
+  int phase_bits = 0;
+  for (int64_t k = 0;; ++k) {
+    const int64_t task = blockIdx.x + k * gridDim.x;
+    if (task >= T) break;
+    const int b = (int)(k % NBUF);
+    if (threadIdx.x == 0) issue(blockIdx.x + (k + NBUF - 1) * gridDim.x, (int)((k + NBUF - 1) % NBUF));
+    mbar_wait(&full[b], (uint32_t)((phase_bits >> b) & 1));
+    phase_bits ^= 1 << b;
+    TA::run_smem(p.a, p, task, 0, 0, bufs + b * BUF, tw, nonfinite, nullptr, nullptr);
+    __syncthreads();
   }
   if (__syncthreads_or(nonfinite) && threadIdx.x == 0) atomicOr(p.flag, 1);
 }

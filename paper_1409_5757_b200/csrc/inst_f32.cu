@@ -62,6 +62,29 @@ bool get_staged_wide_f32(int rho_b, KernelInfo* out) {
 }
 #undef SW
 
+// warp-specialised 32 KB tiles: 1 producer + 8 consumer warps x 16 elements,
+// 3 TMA buffers, 2 CTAs per SM (16 consumer warps per SM)
+template <int RHO> using WS32 = Tile<float, RHO, 256 / RHO, 256, false, 1, 32, 1, true>;
+#define SW3(rb) case rb: *out = make_info<float, WS32<256>, WS32<rb>, true, false, 3>(); return true;
+bool get_staged_ws32_f32(int rho_b, KernelInfo* out) {
+  switch (rho_b) {
+    SW3(8) SW3(16) SW3(32) SW3(64) SW3(128) SW3(256)
+    default: return false;
+  }
+}
+#undef SW3
+
+// TMA-prefetching direct tiles (64 KB, 512 threads x 16 elements, 3 buffers)
+template <int RHO> using TD = Tile<float, RHO, 512 / RHO, 512, false, 1, 0, 0, true>;
+#define DT(r) case r: *out = make_info<float, TD<r>, NoTile, false, false, 3, false, true>(); return true;
+bool get_direct_tp_f32(int rho, KernelInfo* out) {
+  switch (rho) {
+    DT(16) DT(32) DT(64) DT(128) DT(256) DT(512)
+    default: return false;
+  }
+}
+#undef DT
+
 // TMA-prefetching tiles: 512 threads x 16 elements, 3 buffers in flight
 template <int RHO> using TP16 = Tile<float, RHO, 512 / RHO, 512, false, 1, 0, 0, true>;
 #define ST3(rb) case rb: *out = make_info<float, TP16<256>, TP16<rb>, false, false, 3, true>(); return true;
