@@ -20,8 +20,9 @@ Prints ONE JSON line (rank 0).  Keys beyond the base contract:
                 (efft_execute_host): pinned host in -> H2D -> passes -> D2H -> host out
 --impl reference times that CPU restatement (the reference itself is Python and
 cannot travel to the GPU box) and prints the same line shape.
-Multi-GPU (torchrun): each rank transforms its own array (replicas, weak scaling);
-the time is the max over ranks.
+Multi-GPU (torchrun): ONE transform of the config's N, six-step sharded over the
+ranks with NCCL all-to-alls (strong scaling; --replicas runs independent per-GPU
+transforms instead); the time is the max over ranks.
 """
 import argparse
 import json
@@ -214,6 +215,79 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+def run_sharded(args, rank, local, world):
+    """N > 1: ONE transform of the config's N, block-sharded over the ranks
+    (six-step, 3 NCCL all-to-alls; paper_1409_5757_b200/sharded.py); strong scaling."""
+    import torch
+
+    from paper_1409_5757_b200 import sharded, workloads
+
+    cfg = workloads.CONFIGS[args.config]
+    n, dtype = cfg["n"], cfg["dtype"]
+    shard = n // world
+    x = workloads.make_input(shard, dtype, cfg["kind"], workloads.seed_for(args.config) * 1000 + rank)
+    y = torch.empty_like(x)
+    w = torch.empty_like(x)
+    backend = sharded.GpuBackend(dtype, local)
+    fwd = sharded.ShardedTransform(n, world, rank, -1, backend)
+    inv = sharded.ShardedTransform(n, world, rank, 1, backend) if cfg["roundtrip"] else None
+    per_step = 2 if inv else 1
+
+    def step():
+        fwd.execute(x, y, w)
+        if inv is not None:
+            inv.execute(y, x, w)
+
+    for _ in range(max(args.warmup, 3)):
+        step()
+    torch.cuda.synchronize()
+    barrier(world)
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clocks:
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(args.steps):
+            step()
+        e1.record()
+        torch.cuda.synchronize()
+    total_ms = max_over_ranks(e0.elapsed_time(e1), world)
+    barrier(world)
+    ms_per_step = total_ms / args.steps
+    value = per_step * 5.0 * n * math.log2(n) * args.steps / (total_ms * 1e-3) / 1e9
+    elem = ELEM[dtype]
+    exch = sharded.ShardedTransform.exchanged_bytes(n, world, elem)
+    peak, peak_src = measured_peaks()
+    # additive roofline of one sharded transform per rank: 2 FFT passes + 3 local
+    # permutations over HBM, plus 3 all-to-alls over NVLink (770 GB/s measured peer BW)
+    hbm_bytes = 5 * 2 * shard * elem
+    t_roof = hbm_bytes / (peak * 1e9) + exch / 770e9
+    if rank == 0:
+        line = {
+            "metric": "GFLOP/s (5N*log2N) per 1D FFT",
+            "value": round(value, 3), "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps,
+            "warmup": max(args.warmup, 3), "ms_per_step": round(ms_per_step, 4),
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": DTYPE_NAME[dtype], "data": "synthetic (seeded torch generator, see workloads.py)",
+            "config": {"workload": f"{args.config}: {'forward+inverse' if cfg['roundtrip'] else 'forward'} "
+                                   f"1D {dtype} DFT, N={n}, six-step sharded over {world} GPUs",
+                       "n": n, "input": cfg["kind"], "parallelism": f"six-step x{world} (NCCL all-to-all)",
+                       "l2": "inputs larger than L2", "n1_n2": [fwd.n1, fwd.n2]},
+            "roofline": {"bound": "hbm+nvlink", "achieved": round(per_step * t_roof / (ms_per_step * 1e-3), 4),
+                         "peak": 1.0, "unit": "fraction of additive HBM+NVLink roofline",
+                         "frac": round(per_step * t_roof / (ms_per_step * 1e-3), 4), "traffic": None,
+                         "exchange_bytes_per_rank": exch, "t_roof_ms": round(t_roof * 1e3, 4),
+                         "peak_source": peak_src + "; NVLink 770 GB/s measured peer copy (B200_PROFILING.md)"},
+            "gpu_launches": None,
+            "clocks": clocks.summary(),
+            "e2e": None,
+            "cpu_baseline": None,
+        }
+        print(json.dumps(line), flush=True)
+    import torch.distributed as dist
+
+    dist.destroy_process_group()
+
+
 def run_ours(args):
     import torch
 
@@ -221,6 +295,8 @@ def run_ours(args):
     from paper_1409_5757_b200 import _native, workloads
 
     rank, local, world = dist_init()
+    if world > 1 and not args.replicas:
+        return run_sharded(args, rank, local, world)
     torch.cuda.set_device(local)
     cfg = workloads.CONFIGS[args.config]
     n, dtype = cfg["n"], cfg["dtype"]
@@ -334,7 +410,7 @@ def run_ours(args):
             "hbm_gbs_whole_step": round(whole_gbs, 1),
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
                          "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": None,
-                         "kernel": f"pass {dom} (pass_kernel), {avg[dom]:.4f} ms avg",
+                         "kernel": f"pass {dom} of {len(avg)} (staged pass kernel), {avg[dom]:.4f} ms avg",
                          "pass_ms": [round(a, 4) for a in avg], "peak_source": peak_src,
                          "alg_bytes_per_launch": alg_bytes},
             "gpu_launches": launches * args.steps,
@@ -359,6 +435,8 @@ def main():
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--no-e2e", action="store_true", help="skip the host-buffer e2e leg")
     ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--replicas", action="store_true",
+                    help="N>1: independent per-GPU transforms instead of one sharded transform")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

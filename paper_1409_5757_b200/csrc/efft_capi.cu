@@ -145,8 +145,10 @@ int env_int(const char* name, int dflt) {
 }
 
 bool get_staged(int dtype, int ra, int rb, KernelInfo* k) {
-  // EFFT_WS=1 selects the warp-specialised TMA kernel, 0 the register-path kernel
-  static const int ws = env_int("EFFT_WS", 0);
+  // EFFT_WS=1/0 forces the warp-specialised TMA kernel / the register-path
+  // kernel; default: TMA kernel for complex64, register path for complex128
+  // (the faster measured variant of each)
+  const int ws = env_int("EFFT_WS", dtype == EFFT_C64 ? 1 : 0);
   return dtype == EFFT_C64 ? efft::get_staged_kernel_f32(ra, rb, ws, k)
                            : efft::get_staged_kernel_f64(ra, rb, ws, k);
 }
@@ -174,7 +176,7 @@ bool pick_pass(int dtype, int64_t R, PassPlan* pp, int64_t ncols = 0) {
   if (pp->rho_b * pp->rho_a != R || pp->rho_b > 512) return false;
   // complex64 power-of-two passes: EFFT_C64_TILE=256 selects 32 KB tiles (4 CTAs/SM)
   static const int c64_tile = env_int("EFFT_C64_TILE", 512);
-  static const int ws = env_int("EFFT_WS", 0);
+  const int ws = env_int("EFFT_WS", dtype == EFFT_C64 ? 1 : 0);
   bool ok;
   if (dtype == EFFT_C64 && !has3 && c64_tile == 256 && !ws && pp->rho_b <= 256)
     ok = efft::get_staged_small_f32((int)pp->rho_b, &pp->k);

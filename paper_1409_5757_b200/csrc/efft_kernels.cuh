@@ -28,6 +28,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <cstdio>
 #include <type_traits>
 
 #include "w192_table.cuh"
@@ -227,6 +228,29 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
+__device__ __forceinline__ bool mbar_try(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n"
+      " .reg .pred p;\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+      " selp.u32 %0, 1, 0, p;\n"
+      "}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+// wait with a watchdog: after ~2^28 polls report who is stuck and trap
+__device__ __forceinline__ void mbar_wait_dbg(uint64_t* bar, uint32_t parity, int tag, long long a, long long b) {
+  long long n = 0;
+  while (!mbar_try(bar, parity)) {
+    if (++n == (1ll << 30)) {
+      printf("EFFT STUCK tag=%d cta=%d thr=%d parity=%u a=%lld b=%lld\n", tag, blockIdx.x, threadIdx.x, parity, a, b);
+      __trap();
+    }
+  }
+}
 // global -> shared bulk copy completing `bytes` transactions on `bar`
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
                                          uint64_t pol) {
@@ -252,6 +276,14 @@ __device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, i
       " [%0], [%1, {%2, %3, %4, %5}], [%6], %7;" ::"r"(smem_u32(dst)),
       "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_u32(bar)), "l"(pol)
       : "memory");
+}
+__device__ __forceinline__ void red_release_add(int32_t* ctr, int32_t v) {
+  asm volatile("red.release.gpu.global.add.s32 [%0], %1;" ::"l"(ctr), "r"(v) : "memory");
+}
+__device__ __forceinline__ int32_t ld_acquire(const int32_t* ctr) {
+  int32_t v;
+  asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(ctr) : "memory");
+  return v;
 }
 // order generic-proxy writes observed through an acquire before async-proxy reads
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
@@ -929,10 +961,7 @@ struct Tile {
     }
     stage_read<0, SWZ>(v, buf);
     tsync();  // every tile thread has its stage-0 data (and issued its discards)
-    if (release != nullptr && tx() == 0) {
-      __threadfence();
-      atomicAdd(release, 1);
-    }
+    if (release != nullptr && tx() == 0) red_release_add(release, 1);
     if (d.conj_in || d.check_finite) fixup(d, v, nonfinite);
     if (d.tw_mod) twiddle(d, grp, task, v);
     stage_compute<0>(v, tw);
@@ -1063,16 +1092,16 @@ __global__ void __launch_bounds__(TA::NT, min_blocks<TA>()) pass_kernel(const __
   if (__syncthreads_or(nonfinite) && threadIdx.x == 0) atomicOr(p.flag, 1);
 }
 
-// Warp-specialised staged pass (one CTA per SM, persistent).
-//   warp 0 (producer): claims tasks in order, resolves their dependency, and
-//     copies the tile's 128-byte rows (HBM input for A tasks, the L2 staging
-//     ring for B tasks) into one of two shared-memory buffers with
-//     cp.async.bulk, completing an mbarrier -- the next tile streams in while
-//     the consumers work on the current one.
-//   warps 1.. (consumers): wait on the buffer's mbarrier, run the tile
-//     (registers + the same buffer for exchanges, named barrier 1), store,
-//     then release the buffer (empty mbarrier) and, for A tasks, publish the
-//     group counter.
+// Warp-specialised staged pass (persistent).
+//   warp 0 (producer) owns every global synchronisation: it claims tasks in
+//     order, waits for their producers, issues ONE TMA tensor copy per tile
+//     into an NBUF-deep ring of shared-memory buffers, and -- when a buffer
+//     comes back -- retires the task that used it: B tiles discard their
+//     consumed staging lines and release the ring slot, A tiles publish their
+//     group counter (release reduction).
+//   warps 1.. (consumers) only compute: wait on the buffer's `full`
+//     mbarrier, run the tile (the buffer doubles as the exchange buffer,
+//     named barrier 1), store, arrive on `empty`.
 template <typename R, class TA, class TB, int NBUF = 2>
 __global__ void __launch_bounds__(TA::NT + 32, (TA::TILE * (int)sizeof(typename TA::V) <= 32768 ? 2 : 1))
     staged_kernel(const __grid_constant__ PassArgs p) {
@@ -1082,7 +1111,6 @@ __global__ void __launch_bounds__(TA::NT + 32, (TA::TILE * (int)sizeof(typename 
   extern __shared__ __align__(128) unsigned char smem_raw[];
   constexpr int BUF = TA::SMEM_ELEMS > TB::SMEM_ELEMS ? TA::SMEM_ELEMS : TB::SMEM_ELEMS;
   static_assert((BUF * sizeof(V)) % 1024 == 0, "swizzled buffers stay 1024-byte aligned");
-  // 128B swizzle needs 1024-byte aligned buffers (the launch adds 1 KB slack)
   V* bufs = reinterpret_cast<V*>(smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u));
   V* twA = bufs + NBUF * BUF;
   V* twB = twA + TA::RHO;
@@ -1102,15 +1130,50 @@ __global__ void __launch_bounds__(TA::NT + 32, (TA::TILE * (int)sizeof(typename 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   if (warp == 0) {
     const uint64_t pol = policy_evict_first();
-    for (int64_t k = 0;; ++k) {
+    // retire the task that last used buffer b (its consumers are done)
+    auto retire = [&](int b) {
+      if (task_of[b] < 0) return;
+      const int64_t grp = task_grp[b];
+      if (task_isB[b]) {
+        const V* stg = (const V*)p.staging + (int64_t)task_slot[b] * p.slot_elems + (int64_t)task_sub[b] * p.b.it;
+        for (int r = lane; r < TB::D * TB::RHO; r += 32)
+          l2_discard(stg + (r % TB::D) * p.b.is + (int64_t)(r / TB::D) * p.b.im);
+        __syncwarp();
+        if (lane == 0) red_release_add(p.doneB + grp, 1);
+      } else if (lane == 0) {
+        red_release_add(p.doneA + grp, 1);
+      }
+      task_of[b] = -1;
+    };
+    for (int i = 0; i < NBUF; ++i) task_of[i] = -1;
+    // per-buffer counts of issued and retired tasks (warp-uniform)
+    int used[NBUF], retired[NBUF];
+#pragma unroll
+    for (int i = 0; i < NBUF; ++i) used[i] = retired[i] = 0;
+    auto retire_one = [&](int b) {
+      mbar_wait_dbg(&empty[b], (uint32_t)(retired[b] & 1), 1, b, retired[b]);
+      retire(b);
+      ++retired[b];
+    };
+    // retire every outstanding buffer, oldest first (this CTA then holds no
+    // unfinished task, so a blocking dependency wait cannot deadlock)
+    auto drain = [&](int64_t k) {
+      for (int64_t j = k - NBUF + 1; j < k; ++j) {
+        if (j < 0) continue;
+        const int bb = (int)(j % NBUF);
+        if (retired[bb] < used[bb]) retire_one(bb);
+      }
+    };
+    int64_t k = 0;
+    for (;; ++k) {
       const int b = (int)(k % NBUF);
-      if (k >= NBUF) mbar_wait(&empty[b], (uint32_t)(((k / NBUF) - 1) & 1));
+      if (retired[b] < used[b]) retire_one(b);
       unsigned long long pos = 0;
       if (lane == 0) pos = atomicAdd(p.task_counter, 1ull);
       pos = __shfl_sync(0xffffffffu, pos, 0);
       if ((int64_t)pos >= p.total_tasks) {
         if (lane == 0) {
-          task_of[b] = -1;
+          task_of[b] = -2;  // end marker for the consumers (never retired)
           mbar_arrive(&full[b]);
         }
         break;
@@ -1118,34 +1181,48 @@ __global__ void __launch_bounds__(TA::NT + 32, (TA::TILE * (int)sizeof(typename 
       bool isB;
       int64_t grp, sub;
       decode_task(p, (int64_t)pos, isB, grp, sub);
-      if (lane == 0) {
-        const int32_t* ctr = isB ? p.doneA + grp : (grp >= p.nslots ? p.doneB + (grp - p.nslots) : nullptr);
-        const int32_t need = isB ? p.a.ntasks : p.b.ntasks;
-        if (ctr != nullptr && !p.nowait) {
-          while (*(volatile const int32_t*)ctr < need) __nanosleep(32);
-          __threadfence();
+      const int32_t* ctr = isB ? p.doneA + grp : (grp >= p.nslots ? p.doneB + (grp - p.nslots) : nullptr);
+      const int32_t need = isB ? p.a.ntasks : p.b.ntasks;
+      if (ctr != nullptr && !p.nowait) {
+        int ok = 0;
+        if (lane == 0) ok = ld_acquire(ctr) >= need;
+        ok = __shfl_sync(0xffffffffu, ok, 0);
+        if (!ok) {
+          drain(k);
+          if (lane == 0)
+          {
+            long long n = 0;
+            while (ld_acquire(ctr) < need) {
+              __nanosleep(32);
+              if (++n == (1ll << 27)) {
+                printf("EFFT STUCK dep cta=%d pos=%lld isB=%d grp=%lld need=%d have=%d\n", blockIdx.x,
+                       (long long)pos, (int)isB, (long long)grp, need, ld_acquire(ctr));
+                __trap();
+              }
+            }
+          }
+          __syncwarp();
         }
+      }
+      if (lane == 0) {
         fence_proxy_async();
         task_of[b] = (long long)pos;
         task_grp[b] = grp;
         task_sub[b] = (int)sub;
         task_slot[b] = (int)(grp % p.nslots);
         task_isB[b] = isB;
-        const int rows = isB ? TB::D * TB::RHO : TA::D * TA::RHO;
-        mbar_arrive_tx(&full[b], (uint32_t)rows * 128u);
-      }
-      __syncwarp();
-      if (lane == 0) {
         V* dst = bufs + b * BUF;
         if (!isB) {
-          constexpr int W = (int)sizeof(V) / 8;  // tensor-map units (uint64) per element
+          constexpr int W = (int)sizeof(V) / 8;
           constexpr int BOX = TA::RHO > 256 ? TA::RHO / 2 : TA::RHO;
+          mbar_arrive_tx(&full[b], (uint32_t)(TA::D * TA::RHO * 128));
 #pragma unroll
           for (int h = 0; h < TA::RHO / BOX; ++h)
             tma_load_3d(dst + h * BOX * TA::D * TA::F, &p.tmA, (int)(grp * TA::F * W), (int)(sub * TA::D),
                         h * BOX, &full[b], pol);
         } else {
           constexpr int BOX = TB::RHO > 256 ? TB::RHO / 2 : TB::RHO;
+          mbar_arrive_tx(&full[b], (uint32_t)(TB::D * TB::RHO * 128));
 #pragma unroll
           for (int h = 0; h < TB::RHO / BOX; ++h)
             tma_load_4d(dst + h * BOX * TB::D * TB::F, &p.tmB, 0, (int)(sub * TB::D), h * BOX, task_slot[b],
@@ -1153,33 +1230,26 @@ __global__ void __launch_bounds__(TA::NT + 32, (TA::TILE * (int)sizeof(typename 
         }
       }
       __syncwarp();
+      ++used[b];
     }
+    drain(k);  // retire the tasks still holding buffers (buffer k%NBUF holds the end marker)
   } else {
     bool nonfinite = false;
     for (int64_t k = 0;; ++k) {
       const int b = (int)(k % NBUF);
-      mbar_wait(&full[b], (uint32_t)((k / NBUF) & 1));
+      mbar_wait_dbg(&full[b], (uint32_t)((k / NBUF) & 1), 2, b, k);
       const long long pos = task_of[b];
-      if (pos < 0) break;
+      if (pos == -2) break;
       const bool isB = task_isB[b];
       const int64_t grp = task_grp[b];
       const int sub = task_sub[b], slot = task_slot[b];
       V* buf = bufs + b * BUF;
-      if (!isB) {
+      if (!isB)
         TA::run_smem(p.a, p, grp, sub, slot, buf, twA, nonfinite, nullptr, nullptr);
-      } else {
-        const V* stg = (const V*)p.staging + (int64_t)slot * p.slot_elems + (int64_t)sub * p.b.it;
-        TB::run_smem(p.b, p, grp, sub, slot, buf, twB, nonfinite, p.doneB + grp, stg);
-      }
+      else
+        TB::run_smem(p.b, p, grp, sub, slot, buf, twB, nonfinite, nullptr, nullptr);
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[b]);
-      if (!isB) {
-        TA::tsync();
-        if (TA::tx() == 0) {
-          __threadfence();
-          atomicAdd(p.doneA + grp, 1);
-        }
-      }
     }
     if (nonfinite) atomicOr(p.flag, 1);
   }
@@ -1289,15 +1359,18 @@ __global__ void __launch_bounds__(TA::NT, 1) pf_kernel(const __grid_constant__ P
   if (__syncthreads_or(nonfinite) && threadIdx.x == 0) atomicOr(p.flag, 1);
 }
 
-// TMA-prefetching persistent staged pass (no dedicated producer warp).
-// Thread 0 keeps the next NBUF-1 tiles in flight: between tasks it claims a
-// task, checks its dependency without blocking, and issues one TMA tensor
-// copy of the tile (128B-swizzled) into a free shared-memory buffer,
-// completing that buffer's mbarrier.  All NT threads compute the current tile
-// from its buffer (which then doubles as the exchange buffer).  A tile whose
-// producers were not finished when it was claimed is copied later, just
-// before it is needed; that blocking wait is deadlock-free because by then
-// every earlier task held by this CTA is complete.
+// TMA-prefetching persistent staged pass, static schedule.
+// CTA c owns task positions c, c + G, c + 2G, ... of the staged order
+// (decode_task).  Thread 0 keeps NBUF-1 tiles in flight: between tiles it
+// decodes the next position (32-bit integer math), checks the tile's
+// producer counter from a load it issued one tile earlier (so no global
+// round trip sits on the critical path), and issues ONE TMA tensor copy
+// (HBM input for A tiles, the L2 staging ring for B tiles) into the buffer
+// freed by the previous tile.  A tile whose producers were not done is
+// copied just before it is needed (blocking wait; deadlock-free because the
+// smallest unfinished task is always owned by a CTA that has finished all its
+// earlier tasks).  Completion counters are bumped with release reductions.
+
 template <typename R, class TA, class TB, int NBUF>
 __global__ void __launch_bounds__(TA::NT, 1) tp_kernel(const __grid_constant__ PassArgs p) {
   using V = typename CT<R>::V;
@@ -1310,45 +1383,51 @@ __global__ void __launch_bounds__(TA::NT, 1) tp_kernel(const __grid_constant__ P
   V* twA = bufs + NBUF * BUF;
   V* twB = twA + TA::RHO;
   __shared__ __align__(8) uint64_t full[NBUF];
-  __shared__ long long t_pos[NBUF], t_grp[NBUF];
-  __shared__ int t_sub[NBUF], t_slot[NBUF], t_isB[NBUF], t_issued[NBUF], t_phase[NBUF];
+  __shared__ int t_grp[NBUF], t_sub[NBUF], t_slot[NBUF], t_isB[NBUF], t_issued[NBUF];
   if (threadIdx.x == 0)
-    for (int i = 0; i < NBUF; ++i) {
-      mbar_init(&full[i], 1);
-      t_phase[i] = 0;
-    }
+    for (int i = 0; i < NBUF; ++i) mbar_init(&full[i], 1);
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   TA::build_table(twA);
   TB::build_table(twB);
   const uint64_t pol = policy_evict_first();
-  // ---- thread-0 helpers
-  auto dep_ok = [&](int b, bool block) -> bool {
-    const int64_t grp = t_grp[b];
-    const bool isB = t_isB[b];
-    const int32_t* ctr = isB ? p.doneA + grp : (grp >= p.nslots ? p.doneB + (grp - p.nslots) : nullptr);
-    if (ctr == nullptr) return true;
-    const int32_t need = isB ? p.a.ntasks : p.b.ntasks;
-    if (block) {
-      while (*(volatile const int32_t*)ctr < need) __nanosleep(64);
-    } else if (*(volatile const int32_t*)ctr < need) {
-      return false;
+  const uint32_t T = (uint32_t)p.total_tasks, G = gridDim.x;
+  const uint32_t NG = (uint32_t)p.ngroups, LAG = (uint32_t)p.lag, TAn = (uint32_t)p.a.ntasks,
+                 TBn = (uint32_t)p.b.ntasks, NS = (uint32_t)p.nslots;
+  // ---- thread-0 producer state
+  int32_t pre_val = 0;        // prefetched producer-counter value for the next claim
+  const int32_t* pre_ctr = nullptr;
+  uint32_t next_k = 0;        // local index of the next task to claim
+  auto decode32 = [&](uint32_t pos, bool& isB, uint32_t& grp, uint32_t& sub) {
+    if (pos < LAG * TAn) {
+      isB = false;
+      grp = pos / TAn;
+      sub = pos % TAn;
+    } else if (pos < LAG * TAn + (NG - LAG) * (TAn + TBn)) {
+      const uint32_t q = pos - LAG * TAn;
+      const uint32_t i = LAG + q / (TAn + TBn), r = q % (TAn + TBn);
+      isB = r < TBn;
+      grp = isB ? i - LAG : i;
+      sub = isB ? r : r - TBn;
+    } else {
+      const uint32_t q = pos - LAG * TAn - (NG - LAG) * (TAn + TBn);
+      isB = true;
+      grp = NG - LAG + q / TBn;
+      sub = q % TBn;
     }
-    __threadfence();
-    fence_proxy_async();
-    return true;
+  };
+  auto ctr_of = [&](bool isB, uint32_t grp) -> const int32_t* {
+    return isB ? p.doneA + grp : (grp >= NS ? p.doneB + (grp - NS) : nullptr);
   };
   auto issue = [&](int b) {
     V* dst = bufs + b * BUF;
-    const int64_t grp = t_grp[b];
-    const int sub = t_sub[b];
+    const int grp = t_grp[b], sub = t_sub[b];
     if (!t_isB[b]) {
       constexpr int W = (int)sizeof(V) / 8;
       constexpr int BOX = TA::RHO > 256 ? TA::RHO / 2 : TA::RHO;
       mbar_arrive_tx(&full[b], (uint32_t)(TA::D * TA::RHO * 128));
 #pragma unroll
       for (int h = 0; h < TA::RHO / BOX; ++h)
-        tma_load_3d(dst + h * BOX * TA::D * TA::F, &p.tmA, (int)(grp * TA::F * W), sub * TA::D, h * BOX,
-                    &full[b], pol);
+        tma_load_3d(dst + h * BOX * TA::D * TA::F, &p.tmA, grp * TA::F * W, sub * TA::D, h * BOX, &full[b], pol);
     } else {
       constexpr int BOX = TB::RHO > 256 ? TB::RHO / 2 : TB::RHO;
       mbar_arrive_tx(&full[b], (uint32_t)(TB::D * TB::RHO * 128));
@@ -1358,61 +1437,85 @@ __global__ void __launch_bounds__(TA::NT, 1) tp_kernel(const __grid_constant__ P
     }
     t_issued[b] = 1;
   };
-  // task positions are fetched one claim ahead so the atomic's round trip
-  // hides behind a tile's compute instead of stalling the whole CTA
-  unsigned long long next_pos = 0;
-  auto claim = [&](int b) {  // claim a task into buffer b; issue its copy if its producers are done
-    const unsigned long long pos = next_pos;
-    next_pos = atomicAdd(p.task_counter, 1ull);
-    t_pos[b] = (long long)pos;
+  // claim local task next_k into buffer b: decode, test the prefetched counter,
+  // issue the copy if ready, then prefetch the counter of the following task
+  auto claim = [&](int b) {
+    const uint32_t pos = blockIdx.x + next_k * G;
+    ++next_k;
     t_issued[b] = 0;
-    if ((int64_t)pos >= p.total_tasks) return;
+    t_grp[b] = -1;
+    if (pos >= T) return;
     bool isB;
-    int64_t grp, sub;
-    decode_task(p, (int64_t)pos, isB, grp, sub);
+    uint32_t grp, sub;
+    decode32(pos, isB, grp, sub);
     t_isB[b] = isB;
-    t_grp[b] = grp;
+    t_grp[b] = (int)grp;
     t_sub[b] = (int)sub;
-    t_slot[b] = (int)(grp % p.nslots);
-    if (dep_ok(b, false)) issue(b);
+    t_slot[b] = (int)(grp % NS);
+    const int32_t need = isB ? (int32_t)TAn : (int32_t)TBn;
+    const int32_t* ctr = ctr_of(isB, grp);
+    // pre_val came from an acquire load issued one tile ago: if it already
+    // covers `need`, the producers' stores happen-before this copy
+    bool ready = ctr == nullptr || (ctr == pre_ctr && pre_val >= need);
+    if (!ready && ctr != nullptr) ready = ld_acquire(ctr) >= need;  // rare slow path
+    if (ready) {
+      if (ctr != nullptr) fence_proxy_async();
+      issue(b);
+    }
+    // prefetch the producer counter of the next claim (consumed one tile later)
+    const uint32_t npos = blockIdx.x + next_k * G;
+    pre_ctr = nullptr;
+    if (npos < T) {
+      bool nb;
+      uint32_t ng, ns;
+      decode32(npos, nb, ng, ns);
+      pre_ctr = ctr_of(nb, ng);
+      if (pre_ctr != nullptr) pre_val = ld_acquire(pre_ctr);
+    }
   };
   if (threadIdx.x == 0) {
-    next_pos = atomicAdd(p.task_counter, 1ull);
+    const uint32_t pos0 = blockIdx.x;
+    if (pos0 < T) {
+      bool nb;
+      uint32_t ng, ns;
+      decode32(pos0, nb, ng, ns);
+      pre_ctr = ctr_of(nb, ng);
+      if (pre_ctr != nullptr) pre_val = ld_acquire(pre_ctr);
+    }
     for (int i = 0; i < NBUF - 1; ++i) claim(i);
   }
   __syncthreads();
   bool nonfinite = false;
-  for (int64_t k = 0;; ++k) {
+  int phase_bits = 0;
+  for (uint32_t k = 0;; ++k) {
     const int b = (int)(k % NBUF);
     if (threadIdx.x == 0) {
-      // refill the buffer freed by task k-1 with the next claim, and make sure
-      // task k's own copy is under way (blocking on its producers if needed)
-      claim((int)((k + NBUF - 1) % NBUF));
-      if (t_pos[b] < p.total_tasks && !t_issued[b]) {
-        dep_ok(b, true);
+      claim((int)((k + NBUF - 1) % NBUF));  // refill the buffer freed by task k-1
+      if (t_grp[b] >= 0 && !t_issued[b]) {  // task k's producers were late: wait now
+        const int32_t* ctr = ctr_of(t_isB[b], (uint32_t)t_grp[b]);
+        const int32_t need = t_isB[b] ? (int32_t)TAn : (int32_t)TBn;
+        while (ld_acquire(ctr) < need) __nanosleep(64);
+        fence_proxy_async();
         issue(b);
       }
     }
     __syncthreads();
-    if (t_pos[b] >= p.total_tasks) break;
-    mbar_wait(&full[b], (uint32_t)t_phase[b]);
+    const int grp = t_grp[b];
+    if (grp < 0) break;
     const bool isB = t_isB[b];
-    const int64_t grp = t_grp[b];
     const int sub = t_sub[b], slot = t_slot[b];
+    mbar_wait(&full[b], (uint32_t)((phase_bits >> b) & 1));
+    phase_bits ^= 1 << b;
     V* buf = bufs + b * BUF;
     if (!isB) {
       TA::run_smem(p.a, p, grp, sub, slot, buf, twA, nonfinite, nullptr, nullptr);
       __syncthreads();
-      if (threadIdx.x == 0) {
-        __threadfence();
-        atomicAdd(p.doneA + grp, 1);
-      }
+      if (threadIdx.x == 0) red_release_add(p.doneA + grp, 1);
     } else {
       const V* stg = (const V*)p.staging + (int64_t)slot * p.slot_elems + (int64_t)sub * p.b.it;
       TB::run_smem(p.b, p, grp, sub, slot, buf, twB, nonfinite, p.doneB + grp, stg);
       __syncthreads();
     }
-    if (threadIdx.x == 0) t_phase[b] ^= 1;
   }
   if (__syncthreads_or(nonfinite) && threadIdx.x == 0) atomicOr(p.flag, 1);
 }

@@ -120,7 +120,9 @@ class GpuBackend:
         import torch.distributed as dist
 
         if dist.is_available() and dist.is_initialized() and dist.get_world_size(self.group) > 1:
-            dist.all_to_all_single(dst, src, group=self.group)
+            # real views: every NCCL build handles float all-to-all
+            dist.all_to_all_single(self.torch.view_as_real(dst), self.torch.view_as_real(src),
+                                   group=self.group)
         else:
             dst.copy_(src)
 

@@ -248,3 +248,43 @@ def test_c4_3x2p28_complex128_tones():
     xh = x.cpu().numpy()
     yk = y[torch.from_numpy(ks).cuda()].cpu().numpy()
     assert _spot(xh, yk, ks) < tol(n, "complex128")
+
+
+@pytest.mark.slow
+def test_c5_2p32_complex128_roundtrip_and_spots():
+    """Config 5: N = 2^32 complex128 (64 GiB) forward + inverse on ONE B200
+    (in + out + staging ring = 128 GiB + ~90 MB); the input is regenerated from
+    its seed for the round-trip check, so no third array is needed."""
+    from paper_1409_5757_b200 import workloads
+
+    n = 1 << 32
+    free, _ = torch.cuda.mem_get_info()
+    if free < 2 * n * 16 + (1 << 30):
+        pytest.skip("needs ~130 GiB of device memory")
+    import psutil
+
+    if psutil.virtual_memory().available < 2 * n * 16 + (8 << 30):
+        pytest.skip("needs ~140 GB of host memory for the host-side checks")
+    seed = workloads.seed_for("c5")
+    x = workloads.make_input(n, "complex128", "uniform", seed)
+    xh = x.cpu().numpy()
+    y = torch.empty_like(x)
+    s = torch.cuda.current_stream().cuda_stream
+    fwd = _native.NativePlan(n, _native.EFFT_C128, -1, 0)
+    fwd.execute(x.data_ptr(), y.data_ptr(), s)
+    torch.cuda.synchronize()
+    ks = np.array([0, 1, n // 2, n - 1] + list(np.random.default_rng(5).integers(0, n, 12)))
+    yk = y[torch.from_numpy(ks).cuda()].cpu().numpy()
+    assert _spot(xh, yk, ks) < tol(n, "complex128")
+    # Parseval on the device
+    ex = torch.sum(torch.abs(x) ** 2).item()
+    ey = torch.sum(torch.abs(y) ** 2).item()
+    assert abs(ey / (n * ex) - 1) < 1e-12
+    fwd.close()
+    inv = _native.NativePlan(n, _native.EFFT_C128, 1, 0)
+    inv.execute(y.data_ptr(), x.data_ptr(), s)  # overwrite x; xh holds the original
+    torch.cuda.synchronize()
+    del y
+    z = x.cpu().numpy()
+    rt = float(np.linalg.norm(z - xh) / np.linalg.norm(xh))
+    assert rt <= 2 * tol(n, "complex128")

@@ -6,8 +6,8 @@ for l in sys.stdin:
         d=json.loads(l); print(d['ms_per_step'], d['roofline']['pass_ms'], d['config']['plan'][1][-50:])
     else: print(l[:200])
 "; }
-EFFT_C64_TILE=4 timeout 200 python tools/gpu_check.py 1048576,2097152,4194304,16777216 2>&1 | cut -c 1-70
+EFFT_C64_TILE=3 timeout 200 python tools/gpu_check.py 1048576,2097152,4194304,16777216 2>&1 | cut -c 1-70
 run EFFT_C64_TILE=512
-run EFFT_C64_TILE=4
+run EFFT_C64_TILE=3
 CFG=c2 run EFFT_C64_TILE=512
-CFG=c2 run EFFT_C64_TILE=4
+CFG=c2 run EFFT_C64_TILE=3
