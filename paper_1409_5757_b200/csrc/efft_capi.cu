@@ -23,6 +23,7 @@
 
 #include "../../include/efft_b200.h"
 #include "efft_registry.cuh"
+#include "lean.cuh"
 
 using efft::KernelInfo;
 using efft::PassArgs;
@@ -119,6 +120,10 @@ struct efft_plan_s {
   int num_sms = 0;
   bool timing = false;
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};  // launch boundaries
+  // lean path (lean.cu): large power-of-two complex64 transforms
+  bool lean = false;
+  efft::lean::Pass lp[2];
+  float2* lean_t4 = nullptr;  // pass-1 four-step twiddle tables (24 KB)
 };
 
 namespace {
@@ -401,6 +406,19 @@ int build_plan(efft_plan_s* pl) {
     return fail(EFFT_ERR_UNSUPPORTED_SIZE,
                 "n=%lld is not M*2^t with M in {1,3} and n >= 2", (long long)pl->n);
   const int dt = pl->dtype;
+  if (!pl->columns && dt == EFFT_C64 && M == 1 && env_int("EFFT_LEAN", 1)) {
+    int64_t stg = 0;
+    int ecuda = 0;
+    if (efft::lean::plan(pl->n, pl->direction == EFFT_INVERSE, true, (pl->flags & EFFT_FLAG_CHECK_FINITE) != 0,
+                         pl->num_sms, pl->lp, &stg, &ecuda)) {
+      pl->lean = true;
+      pl->npass = 2;
+      pl->staging_bytes = (size_t)stg * sizeof(float2);
+      pl->counter_bytes = (size_t)(pl->lp[0].counter_ints + pl->lp[1].counter_ints) * 4;
+      return EFFT_OK;
+    }
+    if (ecuda) return fail(EFFT_ERR_CUDA, "lean pass setup failed: %s", cudaGetErrorString(cudaGetLastError()));
+  }
   int64_t R1, R2;
   const int64_t dmax = M == 3 ? 384 : 512;
   if (pl->columns) {
@@ -528,6 +546,33 @@ int finish_plan(efft_plan_s* pl) {
     efft_plan_destroy(pl);
     g_err = keep;
     return rc;
+  }
+  if (pl->lean) {
+    if (cudaMalloc((void**)&pl->lean_t4, 3072 * sizeof(float2)) != cudaSuccess) {
+      cudaGetLastError();
+      efft_plan_destroy(pl);
+      return fail(EFFT_ERR_ALLOC, "lean twiddle tables");
+    }
+    efft::lean::build_tables(pl->lean_t4, pl->n, 0);
+    if (cudaDeviceSynchronize() != cudaSuccess) {
+      efft_plan_destroy(pl);
+      return fail(EFFT_ERR_CUDA, "lean twiddle tables: %s", cudaGetErrorString(cudaGetLastError()));
+    }
+    pl->lp[0].a.t4 = pl->lean_t4;
+    if (!efft::lean::encode_stg(pl->lp[0], pl->staging, (int)(pl->staging_bytes / 8 / pl->lp[0].a.slot_elems))) {
+      efft_plan_destroy(pl);
+      return fail(EFFT_ERR_CUDA, "lean staging tensor map");
+    }
+    int64_t off = 0;
+    for (auto& q : pl->lp) {
+      q.a.stg = (float2*)pl->staging;
+      q.a.ctr = reinterpret_cast<unsigned long long*>(pl->counters + off);
+      q.a.doneA = pl->counters + off + 2;
+      q.a.doneB = q.a.doneA + q.a.ngroups;
+      q.a.flag = pl->flag;
+      off += q.counter_ints;
+    }
+    return EFFT_OK;
   }
   for (int p = 0; p < pl->npass; ++p) {
     PassArgs& a = pl->pass[p].args;
@@ -670,7 +715,16 @@ int efft_plan_describe(efft_plan_t pl, char* buf, size_t len) {
            (long long)pl->n, pl->dtype == EFFT_C64 ? "c64" : "c128", pl->direction, pl->npass,
            pl->staging_bytes);
   s += line;
-  for (int p = 0; p < pl->npass; ++p) {
+  for (int p = 0; pl->lean && p < 2; ++p) {
+    const efft::lean::Pass& q = pl->lp[p];
+    snprintf(line, sizeof line,
+             "pass %d: R=%lld lean staged rho_a=256 rho_b=%d stages=[16x16 | %dx16] grid=%d x %d smem=%d "
+             "groups=%d tasks=%lld lag=%d slots=%d\n",
+             p, (long long)q.a.R, q.rb, q.rb / 16, q.grid, q.nt, q.smem, q.a.ngroups, (long long)q.a.total,
+             q.a.lag, q.a.nslots);
+    s += line;
+  }
+  for (int p = 0; !pl->lean && p < pl->npass; ++p) {
     const PassPlan& pp = pl->pass[p];
     std::string st;
     for (int i = 0; i < pp.k.nst_a; ++i) st += (i ? "x" : "") + std::to_string(pp.k.stages_a[i]);
@@ -713,7 +767,18 @@ int efft_execute(efft_plan_t pl, const void* d_in, void* d_out, void* stream) {
   cudaStream_t s = (cudaStream_t)stream;
   CUDA_TRY(cudaSetDevice(pl->device));
   CUDA_TRY(cudaMemsetAsync(pl->counters, 0, pl->counter_bytes, s));
-  for (int p = 0; p < pl->npass; ++p) {
+  for (int p = 0; pl->lean && p < 2; ++p) {
+    if (pl->timing) CUDA_TRY(cudaEventRecord(pl->ev[p], s));
+    efft::lean::Pass& q = pl->lp[p];
+    const void* src = p == 0 ? d_in : d_out;
+    if (q.tmA_src != src && !efft::lean::encode_src(q, src)) return fail(EFFT_ERR_CUDA, "lean tensor map (A)");
+    efft::lean::Args a = q.a;
+    a.src = (const float2*)src;
+    a.dst = (float2*)d_out;
+    q.fn<<<q.grid, q.nt, q.smem, s>>>(a);
+    CUDA_TRY(cudaGetLastError());
+  }
+  for (int p = 0; !pl->lean && p < pl->npass; ++p) {
     if (pl->timing) CUDA_TRY(cudaEventRecord(pl->ev[p], s));
     PassPlan& pp = pl->pass[p];
     const void* src = p == 0 ? d_in : d_out;
@@ -795,6 +860,7 @@ int efft_plan_destroy(efft_plan_t pl) {
   if (pl->staging) cudaFree(pl->staging);
   if (pl->counters) cudaFree(pl->counters);
   if (pl->flag) cudaFree(pl->flag);
+  if (pl->lean_t4) cudaFree(pl->lean_t4);
   if (pl->h_dev_in) cudaFree(pl->h_dev_in);
   if (pl->h_dev_out) cudaFree(pl->h_dev_out);
   delete pl;

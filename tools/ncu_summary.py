@@ -25,6 +25,14 @@ for r in rows[1:]:
 raw = list(csv.reader(io.StringIO(run(["--page", "raw", "--csv"]))))
 if raw:
     h = raw[0]
+    for r in raw[2:]:
+        d = dict(zip(h, r))
+        st = sorted(((float(d[k].replace(",", "") or 0), k.split("stalled_")[1]) for k in h
+                     if k.startswith("smsp__pcsamp_warps_issue_stalled_") and not k.endswith("not_issued")
+                     and d[k].replace(",", "").replace(".", "").isdigit()), reverse=True)
+        print("   stalls:", ", ".join(f"{n}={int(v)}" for v, n in st[:10]))
+if raw:
+    h = raw[0]
     want = [c for c in h if c.startswith(("dram__bytes_read.sum", "dram__bytes_write.sum", "lts__t_bytes.sum",
                                           "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum",
                                           "smsp__average_warp_latency_issue_stalled",
@@ -41,7 +49,7 @@ if len(src) > 2:
     ops, stalls = collections.Counter(), collections.Counter()
     tot = 0
     for r in src[2:]:
-        if len(r) < len(h):
+        if len(r) < len(h) or r[ix["Instructions Executed"]] == "Instructions Executed":
             continue
         s = r[ix["Source"]].strip()
         op = s.split()[0] if s else ""
