@@ -123,7 +123,7 @@ struct efft_plan_s {
   // lean path (lean.cu): large power-of-two complex64 transforms
   bool lean = false;
   efft::lean::Pass lp[2];
-  float2* lean_t4 = nullptr;  // pass-1 four-step twiddle tables (24 KB)
+  void* lean_t4 = nullptr;  // pass-1 four-step twiddle tables (48 / 96 KB)
 };
 
 namespace {
@@ -406,14 +406,14 @@ int build_plan(efft_plan_s* pl) {
     return fail(EFFT_ERR_UNSUPPORTED_SIZE,
                 "n=%lld is not M*2^t with M in {1,3} and n >= 2", (long long)pl->n);
   const int dt = pl->dtype;
-  if (!pl->columns && dt == EFFT_C64 && M == 1 && env_int("EFFT_LEAN", 1)) {
+  if (!pl->columns && M == 1 && env_int("EFFT_LEAN", 1)) {
     int64_t stg = 0;
     int ecuda = 0;
-    if (efft::lean::plan(pl->n, pl->direction == EFFT_INVERSE, true, (pl->flags & EFFT_FLAG_CHECK_FINITE) != 0,
-                         pl->num_sms, pl->lp, &stg, &ecuda)) {
+    if (efft::lean::plan(pl->n, dt == EFFT_C128, pl->direction == EFFT_INVERSE, true,
+                         (pl->flags & EFFT_FLAG_CHECK_FINITE) != 0, pl->num_sms, pl->lp, &stg, &ecuda)) {
       pl->lean = true;
       pl->npass = 2;
-      pl->staging_bytes = (size_t)stg * sizeof(float2);
+      pl->staging_bytes = (size_t)stg * pl->elem;
       pl->counter_bytes = (size_t)(pl->lp[0].counter_ints + pl->lp[1].counter_ints) * 4;
       return EFFT_OK;
     }
@@ -548,24 +548,20 @@ int finish_plan(efft_plan_s* pl) {
     return rc;
   }
   if (pl->lean) {
-    if (cudaMalloc((void**)&pl->lean_t4, 3072 * sizeof(float2)) != cudaSuccess) {
+    if (cudaMalloc(&pl->lean_t4, efft::lean::table_bytes(pl->dtype == EFFT_C128)) != cudaSuccess) {
       cudaGetLastError();
       efft_plan_destroy(pl);
       return fail(EFFT_ERR_ALLOC, "lean twiddle tables");
     }
-    efft::lean::build_tables(pl->lean_t4, pl->n, 0);
+    efft::lean::build_tables(pl->lean_t4, pl->n, pl->dtype == EFFT_C128, 0);
     if (cudaDeviceSynchronize() != cudaSuccess) {
       efft_plan_destroy(pl);
       return fail(EFFT_ERR_CUDA, "lean twiddle tables: %s", cudaGetErrorString(cudaGetLastError()));
     }
     pl->lp[0].a.t4 = pl->lean_t4;
-    if (!efft::lean::encode_stg(pl->lp[0], pl->staging, (int)(pl->staging_bytes / 8 / pl->lp[0].a.slot_elems))) {
-      efft_plan_destroy(pl);
-      return fail(EFFT_ERR_CUDA, "lean staging tensor map");
-    }
     int64_t off = 0;
     for (auto& q : pl->lp) {
-      q.a.stg = (float2*)pl->staging;
+      q.a.stg = pl->staging;
       q.a.ctr = reinterpret_cast<unsigned long long*>(pl->counters + off);
       q.a.doneA = pl->counters + off + 2;
       q.a.doneB = q.a.doneA + q.a.ngroups;
@@ -770,11 +766,9 @@ int efft_execute(efft_plan_t pl, const void* d_in, void* d_out, void* stream) {
   for (int p = 0; pl->lean && p < 2; ++p) {
     if (pl->timing) CUDA_TRY(cudaEventRecord(pl->ev[p], s));
     efft::lean::Pass& q = pl->lp[p];
-    const void* src = p == 0 ? d_in : d_out;
-    if (q.tmA_src != src && !efft::lean::encode_src(q, src)) return fail(EFFT_ERR_CUDA, "lean tensor map (A)");
     efft::lean::Args a = q.a;
-    a.src = (const float2*)src;
-    a.dst = (float2*)d_out;
+    a.src = p == 0 ? d_in : d_out;
+    a.dst = d_out;
     q.fn<<<q.grid, q.nt, q.smem, s>>>(a);
     CUDA_TRY(cudaGetLastError());
   }

@@ -258,6 +258,10 @@ def test_c5_2p32_complex128_roundtrip_and_spots():
     from paper_1409_5757_b200 import workloads
 
     n = 1 << 32
+    import gc
+
+    gc.collect()
+    torch.cuda.empty_cache()
     free, _ = torch.cuda.mem_get_info()
     if free < 2 * n * 16 + (1 << 30):
         pytest.skip("needs ~130 GiB of device memory")

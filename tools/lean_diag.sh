@@ -1,1 +1,1 @@
-for d in 0 1; do echo "== diag $d"; EFFT_LEAN_DIAG=$d timeout 120 python tools/lean_check.py 30 2>&1 | grep "^L="; done
+for d in ${DIAGS:-0 2}; do echo "== diag $d"; EFFT_LEAN_DIAG=$d timeout 120 python tools/lean_check.py ${LOGS:-30} 2>&1 | grep "^L="; done

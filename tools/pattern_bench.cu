@@ -29,7 +29,11 @@ __global__ void __launch_bounds__(256) pat(const float2* __restrict__ src, float
       const int64_t i = u * 256 + hw + 16 * t;  // line id
       int64_t off;
       if (mode == 1) off = (i / R) * 16 + (i % R) * C;
-      else off = i * 16;
+      else if (mode >= 3) {  // W = 2^(mode-2) adjacent column blocks of a row read together
+        const int W = 1 << (mode - 2);
+        const int64_t j = i / W, w = i % W;
+        off = ((j / R) * W + w) * 16 + (j % R) * C;
+      } else off = i * 16;
       v[t] = ld(src + off + lane);
     }
 #pragma unroll
@@ -57,10 +61,10 @@ int main() {
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
-  for (int mode = 0; mode < 3; ++mode)
+  for (int mode = 0; mode < 6; ++mode)
     for (int64_t C : {1ll << 15, 1ll << 12, 1ll << 8})
       for (int occ : {4, 8}) {
-        if (mode == 0 && C != (1ll << 15)) continue;
+        if (mode != 1 && mode != 2 && C != (1ll << 15)) continue;
         const int grid = sms * occ;
         pat<<<grid, 256>>>(a, b, n, C, mode, nunits);
         cudaEventRecord(e0);
