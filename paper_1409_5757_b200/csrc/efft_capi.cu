@@ -120,7 +120,7 @@ struct efft_plan_s {
   int num_sms = 0;
   bool timing = false;
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};  // launch boundaries
-  // lean path (lean.cu): large power-of-two complex64 transforms
+  // lean path (lean.cu): large M * 2^t transforms (both dtypes)
   bool lean = false;
   efft::lean::Pass lp[2];
   void* lean_t4 = nullptr;  // pass-1 four-step twiddle tables (48 / 96 KB)
@@ -406,7 +406,7 @@ int build_plan(efft_plan_s* pl) {
     return fail(EFFT_ERR_UNSUPPORTED_SIZE,
                 "n=%lld is not M*2^t with M in {1,3} and n >= 2", (long long)pl->n);
   const int dt = pl->dtype;
-  if (!pl->columns && M == 1 && env_int("EFFT_LEAN", 1)) {
+  if (!pl->columns && env_int("EFFT_LEAN", 1)) {
     int64_t stg = 0;
     int ecuda = 0;
     if (efft::lean::plan(pl->n, dt == EFFT_C128, pl->direction == EFFT_INVERSE, true,
@@ -714,9 +714,10 @@ int efft_plan_describe(efft_plan_t pl, char* buf, size_t len) {
   for (int p = 0; pl->lean && p < 2; ++p) {
     const efft::lean::Pass& q = pl->lp[p];
     snprintf(line, sizeof line,
-             "pass %d: R=%lld lean staged rho_a=256 rho_b=%d stages=[16x16 | %dx16] grid=%d x %d smem=%d "
+             "pass %d: R=%lld lean staged rho_a=%d rho_b=%d stages=[16x%d | %dx16] grid=%d x %d smem=%d "
              "groups=%d tasks=%lld lag=%d slots=%d\n",
-             p, (long long)q.a.R, q.rb, q.rb / 16, q.grid, q.nt, q.smem, q.a.ngroups, (long long)q.a.total,
+             p, (long long)q.a.R, q.ra, q.rb, q.ra / 16, q.rb / 16, q.grid, q.nt, q.smem, q.a.ngroups,
+             (long long)q.a.total,
              q.a.lag, q.a.nslots);
     s += line;
   }

@@ -84,35 +84,30 @@ __device__ __forceinline__ double2 cscale(double2 v, double2 c) { return make_do
 __device__ __forceinline__ float2 cvt(double2 c, float) { return make_float2((float)c.x, (float)c.y); }
 __device__ __forceinline__ double2 cvt(double2 c, double) { return c; }
 
-// W_R^e, e < R = 256 RB: W_RB^(e >> 8) * W_R^(e & 255)
-template <int RB, typename V>
-__device__ __forceinline__ V w_pass(const V* w256, const V* wlo, int e) {
-  return cmul(w256[(e >> 8) * (256 / RB)], wlo[e & 255]);
-}
 // W_N^e, e < N <= 2^32: three 11-bit levels
 template <typename V>
 __device__ __forceinline__ V w_full(const V* t4, uint32_t e) {
   return cmul(cmul(__ldg(t4 + (e >> 22)), __ldg(t4 + 2048 + ((e >> 11) & 2047))), __ldg(t4 + 4096 + (e & 2047)));
 }
 
-// Position -> (sub-stage, group, task) of the claim order above.
-__device__ __forceinline__ void decode(const Args& a, int lnt, long long pos, int& isB, int& g, int& task) {
-  const long long L = a.lag, nt = a.nt, G = a.ngroups;
-  if (pos < L * nt) {
+// Position -> (sub-stage, group, task) of the claim order above (thread 0 only).
+__device__ __forceinline__ void decode(const Args& a, uint32_t pos, int& isB, int& g, int& task) {
+  const uint32_t L = a.lag, na = a.ntA, nb = a.ntB, per = na + nb, G = a.ngroups;
+  if (pos < L * na) {
     isB = 0;
-    g = (int)(pos >> lnt);
-    task = (int)(pos & (nt - 1));
-  } else if (pos < L * nt + (G - L) * 2 * nt) {
-    const long long q = pos - L * nt;
-    const long long i = L + (q >> (lnt + 1)), r = q & (2 * nt - 1);
-    isB = r < nt;
+    g = (int)(pos / na);
+    task = (int)(pos % na);
+  } else if (pos < L * na + (G - L) * per) {
+    const uint32_t q = pos - L * na;
+    const uint32_t i = L + q / per, r = q % per;
+    isB = r < nb;
     g = (int)(isB ? i - L : i);
-    task = (int)(r & (nt - 1));
+    task = (int)(isB ? r : r - nb);
   } else {
-    const long long q = pos - L * nt - (G - L) * 2 * nt;
+    const uint32_t q = pos - L * na - (G - L) * per;
     isB = 1;
-    g = (int)(G - L + (q >> lnt));
-    task = (int)(q & (nt - 1));
+    g = (int)(G - L + q / nb);
+    task = (int)(q % nb);
   }
 }
 
@@ -138,77 +133,89 @@ struct Sync {
   }
 };
 
-// B tile of the transposing pass: task -> (ks, h, jblk); kt = h F + lane
-template <int F>
+// B tile of the transposing pass: task -> (ks, h, jblk); kt = h F + lane, ks < S
+template <int F, int S>
 __device__ __forceinline__ void t1_task(int task, int& ks, int& h, int& jblk) {
-  ks = task & 15;
-  h = (task >> 4) % (16 / F);
-  jblk = (task >> 4) / (16 / F);
+  ks = task % S;
+  h = (task / S) % (16 / F);
+  jblk = (task / S) / (16 / F);
 }
 
 // staging element offset of a B tile's load (dl, q) for this thread
-template <typename R, int RB, bool T1>
+template <typename R, int RA, int RB, bool T1>
 __device__ __forceinline__ int b_line(int task, int dl, int p, int q, int lane) {
-  constexpr int F = LT<R>::F, QB = RB / 16, DB = 16 / QB;
+  constexpr int F = LT<R>::F, QB = RB / 16, DB = 16 / QB, S = RA / 16;
   const int ja = p + 16 * q;
   if constexpr (T1) {
     int ks, h, jblk;
-    t1_task<F>(task, ks, h, jblk);
-    return (((jblk * DB + dl) * RB + ja) * 16 + ks) * 16 + h * F + lane;
+    t1_task<F, S>(task, ks, h, jblk);
+    return (((jblk * DB + dl) * RB + ja) * S + ks) * 16 + h * F + lane;
   } else {
     return ((task * DB + dl) * RB + ja) * F + lane;
   }
 }
 
-template <typename R, int RB, bool T1, int MINB>
+// A tiles: RA = 16 S points (S = 16, or 12 for the 3 * 2^k family); B tiles:
+// RB = 16 QB points.  R = RA * RB.
+template <typename R, int RA, int RB, bool T1, int MINB>
 __global__ void __launch_bounds__(LT<R>::NT, MINB) lean_pass(const __grid_constant__ Args a) {
   using V = typename LT<R>::V;
   constexpr int F = LT<R>::F, NT = LT<R>::NT, PITCH = LT<R>::PITCH;
-  constexpr int QB = RB / 16, DB = 16 / QB;
+  constexpr int S = RA / 16, QB = RB / 16, DB = 16 / QB;
   extern __shared__ __align__(128) unsigned char smraw[];
   V* xb = reinterpret_cast<V*>(smraw);
-  V* w256 = xb + LT<R>::XB;
-  V* wlo = w256 + 256;
-  __shared__ int s_ready;
-  __shared__ long long s_cur, s_nxt;
+  V* w256 = xb + LT<R>::XB;  // W_256^i      (B inner twiddle, W_RB = W_256^(256/RB))
+  V* wlo = w256 + 256;       // W_R^i, i < 256
+  // W_(R/256)^i, i < R/256 and W_RA^i, i < RA (A inner twiddle): own tables
+  // only when RA = 192; for RA = 256 both are strided views of W_256
+  V* whi = RA == 256 ? w256 : wlo + 256;
+  V* wa = RA == 256 ? w256 : wlo + 512;
+  constexpr int HS = RA == 256 ? 256 / RB : 1;  // stride of whi
+  __shared__ int s_ready, s_isB[2], s_g[2], s_task[2];
+  __shared__ long long s_pos[2];
   const int tid = threadIdx.x, lane = tid % F, r = tid / F;
-  const V* src = reinterpret_cast<const V*>(a.src);
-  V* dst = reinterpret_cast<V*>(a.dst);
-  V* stg = reinterpret_cast<V*>(a.stg);
-  const V* t4 = reinterpret_cast<const V*>(a.t4);
-  const V cin = cvt(a.cin, R()), cout = cvt(a.cout, R());
+  // kernel parameters stay in the constant bank (read at use, no registers held)
+#define SRC reinterpret_cast<const V*>(a.src)
+#define DST reinterpret_cast<V*>(a.dst)
+#define STG reinterpret_cast<V*>(a.stg)
+#define T4 reinterpret_cast<const V*>(a.t4)
   for (int i = tid; i < 256; i += NT) {
     w256[i] = to_v(wroot(i, 256), R());
     wlo[i] = to_v(wroot(i, a.R), R());
+    if constexpr (RA != 256) {
+      whi[i] = to_v(wroot(i, a.R / 256), R());
+      wa[i] = to_v(wroot(i, RA), R());
+    }
   }
-  const int lnt = __ffs(a.nt) - 1;
   Sync sy{nullptr};
-  auto dep_b = [&](long long pos, const int32_t*& c) -> bool {  // is `pos` a B task (c: its producers)?
-    if (pos >= a.total) return false;
-    int isB, g, task;
-    decode(a, lnt, pos, isB, g, task);
-    c = a.doneA + g;
-    return isB;
+  // thread 0: publish the claim `pos` into slot b (decoded once, read by all)
+  auto publish = [&](int b, long long pos) {
+    s_pos[b] = pos;
+    if (pos < a.total) {
+      int isB, g, task;
+      decode(a, (uint32_t)pos, isB, g, task);
+      s_isB[b] = isB;
+      s_g[b] = g;
+      s_task[b] = task;
+    }
   };
+  int cb = 0;  // slot of the current task (the other holds the next)
   if (tid == 0) {
-    s_cur = (long long)atomicAdd(a.ctr, 1ull);
-    s_nxt = (long long)atomicAdd(a.ctr, 1ull);
-    const int32_t* c;
-    s_ready = !dep_b(s_cur, c) || ld_acquire(c) >= a.nt;
+    publish(0, (long long)atomicAdd(a.ctr, 1ull));
+    publish(1, (long long)atomicAdd(a.ctr, 1ull));
+    s_ready = s_pos[0] >= a.total || !s_isB[0] || ld_acquire(a.doneA + s_g[0]) >= a.ntA;
   }
   __syncthreads();
   bool nf = false;
   for (;;) {
-    const long long pos = s_cur;
-    if (pos >= a.total) break;
-    int isB, g, task;
-    decode(a, lnt, pos, isB, g, task);
+    if (s_pos[cb] >= a.total) break;
+    const int isB = s_isB[cb], g = s_g[cb], task = s_task[cb];
     const int slot = g % a.nslots;
-    V* sp = stg + (int64_t)slot * a.slot_elems;
+    V* sp = STG + (int64_t)slot * a.slot_elems;
     if (isB && !s_ready) {  // rare: the producers of this B tile were late
       if (tid == 0) {
         sy.flush();
-        sy.spin(a.doneA + g, a.nt, 1);
+        sy.spin(a.doneA + g, a.ntA, 1);
       }
       __syncthreads();
     }
@@ -217,24 +224,22 @@ __global__ void __launch_bounds__(LT<R>::NT, MINB) lean_pass(const __grid_consta
 #pragma unroll
       for (int dl = 0; dl < DB; ++dl)
 #pragma unroll
-        for (int q = 0; q < QB; ++q) v[dl * QB + q] = ld_staging(sp + b_line<R, RB, T1>(task, dl, r, q, lane));
-    } else {  // A: jb = s + 16 t with s = r
+        for (int q = 0; q < QB; ++q) v[dl * QB + q] = ld_staging(sp + b_line<R, RA, RB, T1>(task, dl, r, q, lane));
+    } else if (r < S) {  // A: jb = s + S t with s = r
       const uint64_t pol = policy_evict_first();
-      const V* p0 = src + (int64_t)g * F + lane + a.LS * (int64_t)(task + RB * r);
-      const int64_t step = a.LS * (int64_t)(RB * 16);
+      const V* p0 = SRC + (int64_t)g * F + lane + a.LS * (int64_t)(task + RB * r);
+      const int64_t step = a.LS * (int64_t)(RB * S);
 #pragma unroll
       for (int t = 0; t < 16; ++t) v[t] = ld_hbm(p0 + t * step, pol);
     }
     // thread 0: claim the task after next; acquire-probe the next task's
     // producers and this A task's staging slot (latency hidden behind the loads)
-    int32_t nxt_val = 0, slot_val = a.nt;
-    bool nxt_isB = false;
+    int32_t nxt_val = 0, slot_val = a.ntB;
     long long claim2 = 0;
     if (tid == 0) {
       claim2 = (long long)atomicAdd(a.ctr, 1ull);
-      const int32_t* nc = nullptr;
-      nxt_isB = dep_b(s_nxt, nc);
-      if (nxt_isB) nxt_val = ld_acquire(nc);
+      const int nb = cb ^ 1;
+      if (s_pos[nb] < a.total && s_isB[nb]) nxt_val = ld_acquire(a.doneA + s_g[nb]);
       if (!isB && g >= a.nslots) slot_val = ld_acquire(a.doneB + (g - a.nslots));
     }
     if (isB) {
@@ -244,13 +249,14 @@ __global__ void __launch_bounds__(LT<R>::NT, MINB) lean_pass(const __grid_consta
         int kb;
         if constexpr (T1) {
           int ks, h, jblk;
-          t1_task<F>(task, ks, h, jblk);
+          t1_task<F, S>(task, ks, h, jblk);
           kb = h * F + lane + 16 * ks;
         } else {
           kb = task * DB + dl;
         }
-        V w = w_pass<RB>(w256, wlo, r * kb);
-        const V st = w_pass<RB>(w256, wlo, (16 * kb) & (256 * RB - 1));
+        const int e0 = r * kb, es = 16 * kb;  // < R
+        V w = cmul(whi[(e0 >> 8) * HS], wlo[e0 & 255]);
+        const V st = cmul(whi[(es >> 8) * HS], wlo[es & 255]);
 #pragma unroll
         for (int q = 0; q < QB; ++q) {
           v[dl * QB + q] = cmul(v[dl * QB + q], w);
@@ -272,24 +278,24 @@ __global__ void __launch_bounds__(LT<R>::NT, MINB) lean_pass(const __grid_consta
       // the consumed staging lines leave L2 without write-back: F lanes share
       // a line, lane i drops the lines of its loads i, i + F, ...
 #pragma unroll
-      for (int i = lane; i < 16; i += F) l2_discard(sp + b_line<R, RB, T1>(task, i / QB, r, i % QB, 0));
+      for (int i = lane; i < 16; i += F) l2_discard(sp + b_line<R, RA, RB, T1>(task, i / QB, r, i % QB, 0));
 #pragma unroll
       for (int dl = 0; dl < DB; ++dl)
 #pragma unroll
         for (int k = 0; k < QB; ++k) xb[((dl * QB + k) * 16 + r) * F + lane] = v[dl * QB + P<QB>(k)];
-    } else {
-      // ---- sub-stage A, stage 0: 16-point DFT over t, W_256^(s kt)
+    } else if (r < S) {
+      // ---- sub-stage A, stage 0: 16-point DFT over t, W_RA^(s kt)
       if (a.check_finite) {
 #pragma unroll
         for (int t = 0; t < 16; ++t) nf |= !(isfinite(v[t].x) && isfinite(v[t].y));
       }
       if constexpr (T1) {
 #pragma unroll
-        for (int t = 0; t < 16; ++t) v[t] = cscale(v[t], cin);
+        for (int t = 0; t < 16; ++t) v[t] = cscale(v[t], cvt(a.cin, R()));
       }
       reg_dft<R, 16>(v);
       {
-        const V* wp = w256;
+        const V* wp = wa;
 #pragma unroll
         for (int k = 1; k < 16; ++k) {
           wp += r;
@@ -301,14 +307,16 @@ __global__ void __launch_bounds__(LT<R>::NT, MINB) lean_pass(const __grid_consta
         if constexpr (T1)
           xb[(r * 16 + k) * PITCH + lane] = v[P<16>(k)];  // [s][kt][j2l]
         else
-          xb[(k * 16 + r) * F + lane] = v[P<16>(k)];  // [kt][s][lane]
-      }
-      if (tid == 0 && slot_val < a.nt) {  // rare: the staging slot is still being read
-        sy.flush();
-        sy.spin(a.doneB + (g - a.nslots), a.nt, 2);
+          xb[(k * S + r) * F + lane] = v[P<16>(k)];  // [kt][s][lane]
       }
     }
-    if (tid == 0) sy.flush();  // release the previous tile (its stores are long done)
+    if (tid == 0) {
+      if (slot_val < a.ntB) {  // rare: this A tile's staging slot is still being read
+        sy.flush();
+        sy.spin(a.doneB + (g - a.nslots), a.ntB, 2);
+      }
+      sy.flush();  // release the previous tile (its stores are long done)
+    }
     __syncthreads();
     if (isB) {
       // ---- sub-stage B, stage 1: 16-point DFT over p; stage-1 thread (lane, dl, kq)
@@ -318,51 +326,55 @@ __global__ void __launch_bounds__(LT<R>::NT, MINB) lean_pass(const __grid_consta
       reg_dft<R, 16>(v);
       const uint64_t pol = policy_evict_first();
       if constexpr (T1) {
-        // y[k1 + R1 j2] = Y W_N^(j2 k1), k1 = kt + 16 ks + 256 kq + 256 QB kp
+        // y[k1 + R1 j2] = Y W_N^(j2 k1), k1 = kt + 16 ks + RA kq + RA QB kp
         int ks, h, jblk;
-        t1_task<F>(task, ks, h, jblk);
+        t1_task<F, S>(task, ks, h, jblk);
         const int j2 = g * F + jblk * DB + dl;
-        const uint32_t c = (uint32_t)(h * F + lane + 16 * ks + 256 * kq);
-        V w = w_full(t4, (uint32_t)((uint64_t)j2 * c));
-        const V st = w_full(t4, (uint32_t)(((uint64_t)j2 * (256 * QB)) & (uint64_t)(a.N - 1)));
-        V* op = dst + (int64_t)j2 * a.R + c;
+        const uint32_t c = (uint32_t)(h * F + lane + 16 * ks + RA * kq);
+        V w = w_full(T4, (uint32_t)((uint64_t)j2 * c));
+        const V st = w_full(T4, (uint32_t)(((uint64_t)j2 * (RA * QB)) % (uint64_t)a.N));
+        V* op = DST + (int64_t)j2 * a.R + c;
 #pragma unroll
         for (int kp = 0; kp < 16; ++kp) {
-          st_hint(op + kp * (256 * QB), cmul(v[P<16>(kp)], w), pol);
+          st_hint(op + kp * (RA * QB), cmul(v[P<16>(kp)], w), pol);
           if (kp < 15) w = cmul(w, st);
         }
       } else {
         const int kb = task * DB + dl;
-        V* op = dst + (int64_t)g * F + lane + a.LS * (int64_t)(kb + 256 * kq);
-        const int64_t step = a.LS * (int64_t)(256 * QB);
+        V* op = DST + (int64_t)g * F + lane + a.LS * (int64_t)(kb + RA * kq);
+        const int64_t step = a.LS * (int64_t)(RA * QB);
 #pragma unroll
-        for (int kp = 0; kp < 16; ++kp) st_hint(op + kp * step, cscale(v[P<16>(kp)], cout), pol);
+        for (int kp = 0; kp < 16; ++kp) st_hint(op + kp * step, cscale(v[P<16>(kp)], cvt(a.cout, R())), pol);
       }
     } else {
-      // ---- sub-stage A, stage 1: 16-point DFT over s -> ks, store to the ring
+      // ---- sub-stage A, stage 1: S-point DFT over s -> ks, store to the ring
       // T0 thread (lane, kt = r): ring [kb][ja][lane], kb = kt + 16 ks
       // T1 thread (kt = tid % 16, j2l = tid / 16): ring [j2l][ja][ks][kt]
       const int kt = T1 ? tid % 16 : r, j2l = tid / 16;
 #pragma unroll
-      for (int u = 0; u < 16; ++u)
-        v[u] = T1 ? xb[(u * 16 + kt) * PITCH + j2l] : xb[(kt * 16 + u) * F + lane];
-      reg_dft<R, 16>(v);
-      const int base = T1 ? (j2l * RB + task) * 256 + kt : (kt * RB + task) * F + lane;
+      for (int u = 0; u < S; ++u) v[u] = T1 ? xb[(u * 16 + kt) * PITCH + j2l] : xb[(kt * S + u) * F + lane];
+      reg_dft<R, S>(v);
+      const int base = T1 ? (j2l * RB + task) * (16 * S) + kt : (kt * RB + task) * F + lane;
       const int step = T1 ? 16 : 16 * RB * F;
       const uint64_t keep = policy_evict_last();
 #pragma unroll
-      for (int ks = 0; ks < 16; ++ks) st_hint(sp + base + ks * step, v[P<16>(ks)], keep);
+      for (int ks = 0; ks < S; ++ks) st_hint(sp + base + ks * step, v[P<S>(ks)], keep);
     }
     if (tid == 0) {
-      s_ready = !nxt_isB || nxt_val >= a.nt;
+      const int nb = cb ^ 1;
+      s_ready = s_pos[nb] >= a.total || !s_isB[nb] || nxt_val >= a.ntA;
       sy.pend = isB ? a.doneB + g : a.doneA + g;
-      s_cur = s_nxt;
-      s_nxt = claim2;
+      publish(cb, claim2);  // the current slot now holds the task after next
     }
+    cb ^= 1;
     __syncthreads();
   }
   if (tid == 0) sy.flush();
   if (__syncthreads_or(nf) && tid == 0) atomicOr(a.flag, 1);
+#undef SRC
+#undef DST
+#undef STG
+#undef T4
 }
 
 template <typename R>
@@ -370,7 +382,7 @@ __global__ void tables_kernel(typename CT<R>::V* t4, int64_t n) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= 3 * 2048) return;
   const int lvl = i >> 11, j = i & 2047;
-  const uint64_t ex = ((uint64_t)j << (11 * (2 - lvl))) & (uint64_t)(n - 1);
+  const uint64_t ex = ((uint64_t)j << (11 * (2 - lvl))) % (uint64_t)n;
   t4[i] = to_v(wroot((int64_t)ex, n), R());
 }
 
@@ -386,33 +398,40 @@ void build_tables(void* t4, int64_t n, int c128, cudaStream_t s) {
     tables_kernel<float><<<24, 256, 0, s>>>((float2*)t4, n);
 }
 
-template <typename R, int MINB>
-static void* pick_m(int rb, bool t1) {
+template <typename R, int RA>
+static void* pick_ra(int rb, bool t1) {
   switch (rb) {
-    case 32: return t1 ? (void*)lean_pass<R, 32, true, MINB> : (void*)lean_pass<R, 32, false, MINB>;
-    case 64: return t1 ? (void*)lean_pass<R, 64, true, MINB> : (void*)lean_pass<R, 64, false, MINB>;
-    case 128: return t1 ? (void*)lean_pass<R, 128, true, MINB> : (void*)lean_pass<R, 128, false, MINB>;
-    case 256: return t1 ? (void*)lean_pass<R, 256, true, MINB> : (void*)lean_pass<R, 256, false, MINB>;
+    case 32: return t1 ? (void*)lean_pass<R, RA, 32, true, 4> : (void*)lean_pass<R, RA, 32, false, 4>;
+    case 64: return t1 ? (void*)lean_pass<R, RA, 64, true, 4> : (void*)lean_pass<R, RA, 64, false, 4>;
+    case 128: return t1 ? (void*)lean_pass<R, RA, 128, true, 4> : (void*)lean_pass<R, RA, 128, false, 4>;
+    case 256: return t1 ? (void*)lean_pass<R, RA, 256, true, 4> : (void*)lean_pass<R, RA, 256, false, 4>;
     default: return nullptr;
   }
 }
 // 4 CTAs per SM for both types (complex64: 64 registers per thread; complex128
 // tiles have half the threads but 128 registers -- a fifth CTA would spill)
 template <typename R>
-static void* pick(int rb, bool t1) {
-  return pick_m<R, 4>(rb, t1);
+static void* pick(int ra, int rb, bool t1) {
+  return ra == 192 ? pick_ra<R, 192>(rb, t1) : pick_ra<R, 256>(rb, t1);
 }
 
 bool plan(int64_t n, int c128, int inverse, bool scale_inverse, bool check_finite, int num_sms, Pass p[2],
           int64_t* staging_elems, int* err_cuda) {
   *err_cuda = 0;
-  if (n <= 0 || (n & (n - 1))) return false;
-  int L = 0;
-  while ((int64_t(1) << L) < n) ++L;
-  if (L < 26 || L > 32) return false;
-  const int L1 = (L + 1) / 2, L2 = L - L1;
-  if (L1 < 13 || L1 > 16 || L2 < 13 || L2 > 16) return false;
-  const int64_t R1 = int64_t(1) << L1, R2 = int64_t(1) << L2;
+  if (n <= 0) return false;
+  int64_t m = n;
+  int t = 0;
+  while ((m & 1) == 0) {
+    m >>= 1;
+    ++t;
+  }
+  if (m != 1 && m != 3) return false;
+  // pass 1: RA1 = 256 (192 when 3 | n), pass 2: RA2 = 256; log2(RB1 RB2) = t - 16 (or t - 14)
+  const int ra1 = m == 3 ? 192 : 256;
+  const int lbs = m == 3 ? t - 14 : t - 16;
+  const int lb1 = (lbs + 1) / 2, lb2 = lbs - lb1;
+  if (lb1 < 5 || lb1 > 8 || lb2 < 5 || lb2 > 8) return false;
+  const int64_t R1 = (int64_t)ra1 << lb1, R2 = int64_t(256) << lb2;
   const int F = c128 ? 8 : 16, NT = 16 * F;
   const size_t elem = c128 ? 16 : 8;
   int64_t stg = 0;
@@ -420,20 +439,22 @@ bool plan(int64_t n, int c128, int inverse, bool scale_inverse, bool check_finit
     Pass& q = p[i];
     const bool t1 = i == 0;
     const int64_t R = t1 ? R1 : R2;
-    q.rb = (int)(R / 256);
-    q.fn = reinterpret_cast<void (*)(Args)>(c128 ? pick<double>(q.rb, t1) : pick<float>(q.rb, t1));
+    q.ra = t1 ? ra1 : 256;
+    q.rb = 1 << (t1 ? lb1 : lb2);
+    q.fn = reinterpret_cast<void (*)(Args)>(c128 ? pick<double>(q.ra, q.rb, t1) : pick<float>(q.ra, q.rb, t1));
     if (!q.fn) return false;
     q.nt = NT;
-    q.smem = (int)((256 * (F + 1) + 512) * elem);
+    q.smem = (int)((256 * (F + 1) + (q.ra == 256 ? 2 : 4) * 256) * elem);
     Args& a = q.a;
     a = Args{};
     a.R = R;
     a.N = n;
     a.LS = t1 ? R2 : R1;
     a.ngroups = (int32_t)((t1 ? R2 : R1) / F);
-    a.nt = q.rb;
+    a.ntA = q.rb;
+    a.ntB = q.ra * q.rb / 256;
     a.slot_elems = (int64_t)F * R;
-    a.total = (int64_t)a.ngroups * 2 * a.nt;
+    a.total = (int64_t)a.ngroups * (a.ntA + a.ntB);
     a.cin = make_double2(1.0, t1 && inverse ? -1.0 : 1.0);
     const double sc = (!t1 && inverse && scale_inverse) ? 1.0 / (double)n : 1.0;
     a.cout = make_double2(sc, (!t1 && inverse) ? -sc : sc);
@@ -450,7 +471,7 @@ bool plan(int64_t n, int c128, int inverse, bool scale_inverse, bool check_finit
     q.grid = occ * num_sms;
     // Claimed tasks in flight span about 3 grids: B(g) is issued `lag` groups
     // after A(g), and A(g) reuses the slot of group g - nslots.
-    const int64_t per = 2 * (int64_t)a.nt;
+    const int64_t per = (int64_t)a.ntA + a.ntB;
     const int64_t window = (4 * (int64_t)q.grid + per - 1) / per;
     int64_t lag = window + 1;
     if (const char* ev = getenv("EFFT_LEAN_LAG")) lag = atoi(ev);

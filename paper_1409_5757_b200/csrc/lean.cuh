@@ -1,13 +1,14 @@
 // lean.cuh -- host-side interface of the lean staged passes (lean.cu).
 //
 // The lean path runs the large power-of-two transforms (complex64 and
-// complex128, N = R1 * R2 with R = 256 * rho_b, rho_b in {32, 64, 128, 256},
-// i.e. 2^26 <= N <= 2^32) as two staged passes of one persistent kernel each:
+// complex128, N = R1 * R2 with R = rho_a * rho_b, rho_a = 256 (or 192 in pass 1
+// for N = 3 * 2^k), rho_b in {32, 64, 128, 256}: 2^26 <= N <= 2^32 and
+// 3 * 2^24 <= N <= 3 * 2^30) as two staged passes of one persistent kernel each:
 //   pass 1: x[j2 + R2*j1] -> y[k1 + R1*j2] (DFT over j1, the four-step twiddle
 //           W_N^(j2*k1) fused into the store, the j2 <-> k1 transpose fused
 //           into sub-stage A's register exchange)
 //   pass 2: y[k1 + R1*j2] -> X[k1 + R1*k2] in place (DFT over j2)
-// Each pass is sub-stage A (256-point DFTs, HBM -> L2 staging ring) and
+// Each pass is sub-stage A (rho_a-point DFTs, HBM -> L2 staging ring) and
 // sub-stage B (rho_b-point DFTs, ring -> HBM); 32 KB tiles, 16 elements per
 // thread, four CTAs per SM.
 #pragma once
@@ -27,8 +28,9 @@ struct Args {
   int64_t R;           // DFT length of the pass (256 * RB)
   int64_t N;           // full transform length (four-step twiddle of pass 1)
   int64_t slot_elems;  // F * R: one column group
-  int64_t total;       // ngroups * 2 * nt tasks
-  int32_t ngroups, nslots, lag, nt;  // nt = tasks per group and sub-stage (RB)
+  int64_t total;       // ngroups * (ntA + ntB) tasks
+  int32_t ngroups, nslots, lag;
+  int32_t ntA, ntB;    // tasks per group: A (RB, one per ja), B (RA * RB / 256)
   unsigned long long* ctr;
   int32_t* doneA;
   int32_t* doneB;
@@ -42,7 +44,7 @@ struct Pass {
   Args a;
   void (*fn)(Args);
   int grid, nt, smem;
-  int rb;
+  int ra, rb;
   int64_t counter_ints;  // 2 (task counter) + 2 * ngroups
 };
 

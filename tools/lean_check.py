@@ -24,11 +24,12 @@ def run(p, x, y, reps=1):
     return e0.elapsed_time(e1) / reps
 
 
-logs = [int(v) for v in sys.argv[1].split(",")] if len(sys.argv) > 1 else [26, 27, 28, 29, 30]
+logs = sys.argv[1].split(",") if len(sys.argv) > 1 else ["26", "27", "28", "29", "30"]
 c128 = len(sys.argv) > 2 and sys.argv[2] == "c128"
 tdt, ndt, esz = (torch.complex128, _native.EFFT_C128, 16) if c128 else (torch.complex64, _native.EFFT_C64, 8)
-for L in logs:
-    n = 1 << L
+for tok in logs:
+    L = int(tok.split("x")[-1])
+    n = (3 if tok.startswith("3x") else 1) << L
     g = torch.Generator(device="cuda").manual_seed(L)
     x = torch.randn(n, dtype=tdt, device="cuda", generator=g)
     y = torch.empty_like(x)
@@ -59,7 +60,7 @@ for L in logs:
         torch.cuda.synchronize()
         rt = rel(z, x)
     gbs = [2 * n * esz / (t * 1e-3) / 1e9 for t in pt]
-    print(f"L={L} lean: {ms:.3f} ms  passes {['%.3f' % t for t in pt]} ms = {['%.0f' % v for v in gbs]} GB/s  "
+    print(f"N={tok} lean: {ms:.3f} ms  passes {['%.3f' % t for t in pt]} ms = {['%.0f' % v for v in gbs]} GB/s  "
           f"err_vs_cufft={err:.3e} roundtrip={rt:.3e}", flush=True)
     del z, x, y
     torch.cuda.empty_cache()
