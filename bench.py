@@ -368,10 +368,17 @@ def run_ours(args):
 
     # e2e through the C-ABI host-buffer entry (rank-local), fewer steps: PCIe bound
     e2e = None
+    x_host = None
     if not args.no_e2e:
         hin = torch.empty(n, dtype=x.dtype, pin_memory=True)
         hout = torch.empty(n, dtype=x.dtype, pin_memory=True)
         hin.copy_(x)
+        if 4 * n * ELEM[dtype] > torch.cuda.mem_get_info()[1] * 0.9:
+            # C5: the host-buffer entry owns its own device in/out arrays; the
+            # device-resident pair of the kernel timing must go first
+            x_host = hin
+            del x, y
+            torch.cuda.empty_cache()
         e2e_steps = max(1, min(args.steps, args.e2e_steps))
         fwd.execute_host(hin.data_ptr(), hout.data_ptr(), sid)  # warm (allocates device buffers)
         torch.cuda.synchronize()
@@ -392,7 +399,7 @@ def run_ours(args):
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        cpu = cpu_baseline(args.config, cfg, x)
+        cpu = cpu_baseline(args.config, cfg, x if x_host is None else x_host)
 
     if rank == 0:
         line = {
@@ -410,7 +417,7 @@ def run_ours(args):
             "hbm_gbs_whole_step": round(whole_gbs, 1),
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
                          "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": None,
-                         "kernel": f"pass {dom} of {len(avg)} (staged pass kernel), {avg[dom]:.4f} ms avg",
+                         "kernel": f"pass {dom} of {len(avg)} (lean_pass kernel), {avg[dom]:.4f} ms avg",
                          "pass_ms": [round(a, 4) for a in avg], "peak_source": peak_src,
                          "alg_bytes_per_launch": alg_bytes},
             "gpu_launches": launches * args.steps,

@@ -114,12 +114,17 @@ __device__ __forceinline__ void decode(const Args& a, uint32_t pos, int& isB, in
 // thread 0's synchronisation state
 struct Sync {
   int32_t* pend;  // completion counter of the finished, not yet released tile
-  __device__ __forceinline__ void flush() {
+  // release pattern: fence.acq_rel then a relaxed add.  The same fence also
+  // completes the acquire of every relaxed probe thread 0 issued before it.
+  __device__ __forceinline__ void fence_release() {
+    asm volatile("fence.acq_rel.gpu;" ::: "memory");
     if (pend != nullptr) {
-      __threadfence();
-      red_release_add(pend, 1);
+      asm volatile("red.relaxed.gpu.global.add.s32 [%0], 1;" ::"l"(pend) : "memory");
       pend = nullptr;
     }
+  }
+  __device__ __forceinline__ void flush() {
+    if (pend != nullptr) fence_release();
   }
   __device__ __forceinline__ void spin(const int32_t* c, int32_t need, int tag) {
     long long n = 0;
@@ -132,6 +137,12 @@ struct Sync {
     }
   }
 };
+
+__device__ __forceinline__ int32_t ld_relaxed(const int32_t* p) {
+  int32_t v;
+  asm volatile("ld.relaxed.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
 
 // B tile of the transposing pass: task -> (ks, h, jblk); kt = h F + lane, ks < S
 template <int F, int S>
@@ -155,8 +166,95 @@ __device__ __forceinline__ int b_line(int task, int dl, int p, int q, int lane) 
   }
 }
 
-// A tiles: RA = 16 S points (S = 16, or 12 for the 3 * 2^k family); B tiles:
-// RB = 16 QB points.  R = RA * RB.
+// Per-CTA task scheduling shared by the tile kernels (see the header comment):
+// dynamic claims two ahead, decoded once by thread 0 into shared memory;
+// acquire probes issued beside the tile loads; release of tile k deferred to
+// the middle of tile k+1.
+struct SchedShared {
+  int ready, isB[2], g[2], task[2];
+  long long pos[2];
+};
+
+struct Sched {
+  SchedShared* sh;
+  int cb = 0;         // slot of the current task (the other holds the next)
+  Sync sy{nullptr};   // thread 0
+  int32_t nxt_val = 0, slot_val = 0;
+  long long claim2 = 0;
+
+  __device__ __forceinline__ void publish(const Args& a, int b, long long pos) {  // thread 0
+    sh->pos[b] = pos;
+    if (pos < a.total) {
+      int isB, g, task;
+      decode(a, (uint32_t)pos, isB, g, task);
+      sh->isB[b] = isB;
+      sh->g[b] = g;
+      sh->task[b] = task;
+    }
+  }
+  __device__ __forceinline__ void init(const Args& a) {  // all threads
+    if (threadIdx.x == 0) {
+      publish(a, 0, (long long)atomicAdd(a.ctr, 1ull));
+      publish(a, 1, (long long)atomicAdd(a.ctr, 1ull));
+      sh->ready = sh->pos[0] >= a.total || !sh->isB[0] || ld_acquire(a.doneA + sh->g[0]) >= a.ntA;
+    }
+    __syncthreads();
+  }
+  // loop top (all threads): the current task, or false when the pass is done.
+  // Thread 0 also claims the task after next and probes (relaxed) the next
+  // task's producers and this A task's staging slot; the fence in
+  // before_exchange() completes those acquires before anything depends on them.
+  __device__ __forceinline__ bool next(const Args& a, int& isB, int& g, int& task) {
+    if (sh->pos[cb] >= a.total) return false;
+    isB = sh->isB[cb];
+    g = sh->g[cb];
+    task = sh->task[cb];
+    if (isB && !sh->ready) {  // rare: the producers of this B tile were late
+      if (threadIdx.x == 0) {
+        sy.flush();
+        sy.spin(a.doneA + g, a.ntA, 1);
+      }
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+      claim2 = (long long)atomicAdd(a.ctr, 1ull);
+      const int nb = cb ^ 1;
+      nxt_val = 0;
+      slot_val = a.ntB;
+      if (sh->pos[nb] < a.total && sh->isB[nb]) nxt_val = ld_relaxed(a.doneA + sh->g[nb]);
+      if (!isB && g >= a.nslots) slot_val = ld_relaxed(a.doneB + (g - a.nslots));
+    }
+    return true;
+  }
+  // thread 0, right after issuing the tile loads: one fence (acquire of the
+  // probes, release of the previous tile).  Warp 0 waits for its loads here
+  // anyway, so the fence costs no extra time on the critical path.
+  __device__ __forceinline__ void after_loads(const Args&, int, int) {
+    if (threadIdx.x == 0) sy.fence_release();
+  }
+  // thread 0, before the exchange barrier: this A tile may store once its
+  // staging slot is free (rarely not yet)
+  __device__ __forceinline__ void before_exchange(const Args& a, int g) {
+    if (threadIdx.x == 0 && slot_val < a.ntB) sy.spin(a.doneB + (g - a.nslots), a.ntB, 2);
+  }
+  __device__ __forceinline__ void end(const Args& a, int isB, int g) {  // all threads
+    if (threadIdx.x == 0) {
+      const int nb = cb ^ 1;
+      sh->ready = sh->pos[nb] >= a.total || !sh->isB[nb] || nxt_val >= a.ntA;
+      sy.pend = isB ? a.doneB + g : a.doneA + g;
+      publish(a, cb, claim2);  // the current slot now holds the task after next
+    }
+    cb ^= 1;
+    __syncthreads();
+  }
+  __device__ __forceinline__ void finish(const Args& a, bool nf) {
+    if (threadIdx.x == 0) sy.flush();
+    if (__syncthreads_or(nf) && threadIdx.x == 0) atomicOr(a.flag, 1);
+  }
+};
+
+// Generic tile kernel: one element per lane.  A tiles: RA = 16 S points
+// (S = 16, or 12 for the 3 * 2^k family); B tiles: RB = 16 QB points.
 template <typename R, int RA, int RB, bool T1, int MINB>
 __global__ void __launch_bounds__(LT<R>::NT, MINB) lean_pass(const __grid_constant__ Args a) {
   using V = typename LT<R>::V;
@@ -171,8 +269,7 @@ __global__ void __launch_bounds__(LT<R>::NT, MINB) lean_pass(const __grid_consta
   V* whi = RA == 256 ? w256 : wlo + 256;
   V* wa = RA == 256 ? w256 : wlo + 512;
   constexpr int HS = RA == 256 ? 256 / RB : 1;  // stride of whi
-  __shared__ int s_ready, s_isB[2], s_g[2], s_task[2];
-  __shared__ long long s_pos[2];
+  __shared__ SchedShared shs;
   const int tid = threadIdx.x, lane = tid % F, r = tid / F;
   // kernel parameters stay in the constant bank (read at use, no registers held)
 #define SRC reinterpret_cast<const V*>(a.src)
@@ -187,38 +284,12 @@ __global__ void __launch_bounds__(LT<R>::NT, MINB) lean_pass(const __grid_consta
       wa[i] = to_v(wroot(i, RA), R());
     }
   }
-  Sync sy{nullptr};
-  // thread 0: publish the claim `pos` into slot b (decoded once, read by all)
-  auto publish = [&](int b, long long pos) {
-    s_pos[b] = pos;
-    if (pos < a.total) {
-      int isB, g, task;
-      decode(a, (uint32_t)pos, isB, g, task);
-      s_isB[b] = isB;
-      s_g[b] = g;
-      s_task[b] = task;
-    }
-  };
-  int cb = 0;  // slot of the current task (the other holds the next)
-  if (tid == 0) {
-    publish(0, (long long)atomicAdd(a.ctr, 1ull));
-    publish(1, (long long)atomicAdd(a.ctr, 1ull));
-    s_ready = s_pos[0] >= a.total || !s_isB[0] || ld_acquire(a.doneA + s_g[0]) >= a.ntA;
-  }
-  __syncthreads();
+  Sched sc{&shs};
+  sc.init(a);
   bool nf = false;
-  for (;;) {
-    if (s_pos[cb] >= a.total) break;
-    const int isB = s_isB[cb], g = s_g[cb], task = s_task[cb];
-    const int slot = g % a.nslots;
-    V* sp = STG + (int64_t)slot * a.slot_elems;
-    if (isB && !s_ready) {  // rare: the producers of this B tile were late
-      if (tid == 0) {
-        sy.flush();
-        sy.spin(a.doneA + g, a.ntA, 1);
-      }
-      __syncthreads();
-    }
+  int isB, g, task;
+  while (sc.next(a, isB, g, task)) {
+    V* sp = STG + (int64_t)(g % a.nslots) * a.slot_elems;
     V v[16];
     if (isB) {
 #pragma unroll
@@ -232,16 +303,7 @@ __global__ void __launch_bounds__(LT<R>::NT, MINB) lean_pass(const __grid_consta
 #pragma unroll
       for (int t = 0; t < 16; ++t) v[t] = ld_hbm(p0 + t * step, pol);
     }
-    // thread 0: claim the task after next; acquire-probe the next task's
-    // producers and this A task's staging slot (latency hidden behind the loads)
-    int32_t nxt_val = 0, slot_val = a.ntB;
-    long long claim2 = 0;
-    if (tid == 0) {
-      claim2 = (long long)atomicAdd(a.ctr, 1ull);
-      const int nb = cb ^ 1;
-      if (s_pos[nb] < a.total && s_isB[nb]) nxt_val = ld_acquire(a.doneA + s_g[nb]);
-      if (!isB && g >= a.nslots) slot_val = ld_acquire(a.doneB + (g - a.nslots));
-    }
+    sc.after_loads(a, isB, g);
     if (isB) {
       // ---- sub-stage B, stage 0: W_R^(ja kb) (exact base and step, recurrence over q)
 #pragma unroll
@@ -310,13 +372,7 @@ __global__ void __launch_bounds__(LT<R>::NT, MINB) lean_pass(const __grid_consta
           xb[(k * S + r) * F + lane] = v[P<16>(k)];  // [kt][s][lane]
       }
     }
-    if (tid == 0) {
-      if (slot_val < a.ntB) {  // rare: this A tile's staging slot is still being read
-        sy.flush();
-        sy.spin(a.doneB + (g - a.nslots), a.ntB, 2);
-      }
-      sy.flush();  // release the previous tile (its stores are long done)
-    }
+    sc.before_exchange(a, g);
     __syncthreads();
     if (isB) {
       // ---- sub-stage B, stage 1: 16-point DFT over p; stage-1 thread (lane, dl, kq)
@@ -360,17 +416,262 @@ __global__ void __launch_bounds__(LT<R>::NT, MINB) lean_pass(const __grid_consta
 #pragma unroll
       for (int ks = 0; ks < S; ++ks) st_hint(sp + base + ks * step, v[P<S>(ks)], keep);
     }
-    if (tid == 0) {
-      const int nb = cb ^ 1;
-      s_ready = s_pos[nb] >= a.total || !s_isB[nb] || nxt_val >= a.ntA;
-      sy.pend = isB ? a.doneB + g : a.doneA + g;
-      publish(cb, claim2);  // the current slot now holds the task after next
-    }
-    cb ^= 1;
-    __syncthreads();
+    sc.end(a, isB, g);
   }
-  if (tid == 0) sy.flush();
-  if (__syncthreads_or(nf) && tid == 0) atomicOr(a.flag, 1);
+  sc.finish(a, nf);
+#undef SRC
+#undef DST
+#undef STG
+#undef T4
+}
+
+// Paired-column complex64 tile kernel (the default for complex64, RA = 256):
+// each thread owns two adjacent columns, so every global and most shared
+// accesses are 16 bytes (8 lanes per 128-byte line: half the memory requests
+// of the one-element-per-lane kernel -- the request rate, not the bytes in
+// flight, bounds a 128-byte-line gather on B200).  32 elements per thread,
+// 128 threads per 4096-element tile, 4 CTAs per SM.
+//   thread (cp = tid % 8: columns 2cp, 2cp+1;  r = tid / 8)
+//   exchange: float4 rows [..][8 pairs]; the transposing one (T1 A) in
+//   8-byte elements, [s][kt][j2] with kt pitch 17 and s pitch 273 (both sides
+//   conflict-free).
+namespace pair {
+constexpr int NT = 128;
+constexpr int XB2 = 16 * 273;  // float2 elements of the exchange buffer (>= 4096)
+
+__device__ __forceinline__ float4 ld16_hbm(const float2* p, uint64_t pol) {
+  float4 r;
+  asm volatile("ld.global.L1::no_allocate.L2::cache_hint.v4.f32 {%0,%1,%2,%3}, [%4], %5;"
+               : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w)
+               : "l"(p), "l"(pol));
+  return r;
+}
+__device__ __forceinline__ float4 ld16_l2(const float2* p) {
+  float4 r;
+  asm volatile("ld.global.cg.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w) : "l"(p));
+  return r;
+}
+__device__ __forceinline__ void st16(float2* p, float2 a, float2 b, uint64_t pol) {
+  st_hint(reinterpret_cast<float4*>(p), make_float4(a.x, a.y, b.x, b.y), pol);
+}
+}  // namespace pair
+
+template <int RB, bool T1>
+__device__ __forceinline__ int pair_b_line(int task, int dl, int p, int q) {
+  constexpr int QB = RB / 16, DB = 16 / QB;
+  const int ja = p + 16 * q;
+  if constexpr (T1)  // ring [j2l][ja][ks][kt]; task = (ks, jblk)
+    return ((((task >> 4) * DB + dl) * RB + ja) * 16 + (task & 15)) * 16;
+  else  // ring [kb][ja][lane]
+    return ((task * DB + dl) * RB + ja) * 16;
+}
+
+template <int RB, bool T1>
+__global__ void __launch_bounds__(pair::NT, 4) lean_pair(const __grid_constant__ Args a) {
+  using V = float2;
+  constexpr int QB = RB / 16, DB = 16 / QB;
+  extern __shared__ __align__(128) unsigned char smraw[];
+  V* xb = reinterpret_cast<V*>(smraw);
+  float4* xq = reinterpret_cast<float4*>(smraw);
+  V* w256 = xb + pair::XB2;
+  V* wlo = w256 + 256;
+  __shared__ SchedShared shs;
+  const int tid = threadIdx.x, cp = tid % 8, r = tid / 8;
+#define SRC reinterpret_cast<const V*>(a.src)
+#define DST reinterpret_cast<V*>(a.dst)
+#define STG reinterpret_cast<V*>(a.stg)
+#define T4 reinterpret_cast<const V*>(a.t4)
+  for (int i = tid; i < 256; i += pair::NT) {
+    w256[i] = to_v(wroot(i, 256), 0.f);
+    wlo[i] = to_v(wroot(i, a.R), 0.f);
+  }
+  Sched sc{&shs};
+  sc.init(a);
+  bool nf = false;
+  int isB, g, task;
+  while (sc.next(a, isB, g, task)) {
+    V* sp = STG + (int64_t)(g % a.nslots) * a.slot_elems;
+    V x[16], y[16];  // columns 2cp (x) and 2cp + 1 (y)
+    if (isB) {
+#pragma unroll
+      for (int dl = 0; dl < DB; ++dl)
+#pragma unroll
+        for (int q = 0; q < QB; ++q) {
+          const float4 t = pair::ld16_l2(sp + pair_b_line<RB, T1>(task, dl, r, q) + 2 * cp);
+          x[dl * QB + q] = make_float2(t.x, t.y);
+          y[dl * QB + q] = make_float2(t.z, t.w);
+        }
+    } else {  // A: jb = s + 16 t with s = r
+      const uint64_t pol = policy_evict_first();
+      const V* p0 = SRC + (int64_t)g * 16 + 2 * cp + a.LS * (int64_t)(task + RB * r);
+      const int64_t step = a.LS * (int64_t)(RB * 16);
+#pragma unroll
+      for (int t = 0; t < 16; ++t) {
+        const float4 u = pair::ld16_hbm(p0 + t * step, pol);
+        x[t] = make_float2(u.x, u.y);
+        y[t] = make_float2(u.z, u.w);
+      }
+    }
+    sc.after_loads(a, isB, g);
+    if (isB) {
+      // ---- B stage 0: W_R^(ja kb) (T0: one kb per dl, shared by the pair;
+      // T1: kb = kt + 16 ks differs between the columns), QB-point DFTs
+#pragma unroll
+      for (int dl = 0; dl < DB; ++dl) {
+        const int kb = T1 ? 2 * cp + 16 * (task & 15) : task * DB + dl;
+        const int e0 = r * kb, es = 16 * kb;  // < R
+        V w = cmul(w256[(e0 >> 8) * (256 / RB)], wlo[e0 & 255]);
+        const V st = cmul(w256[(es >> 8) * (256 / RB)], wlo[es & 255]);
+        if constexpr (T1) {
+          const int e1 = e0 + r, es1 = es + 16;  // kb + 1
+          V w1 = cmul(w256[(e1 >> 8) * (256 / RB)], wlo[e1 & 255]);
+          const V st1 = cmul(w256[(es1 >> 8) * (256 / RB)], wlo[es1 & 255]);
+#pragma unroll
+          for (int q = 0; q < QB; ++q) {
+            x[dl * QB + q] = cmul(x[dl * QB + q], w);
+            y[dl * QB + q] = cmul(y[dl * QB + q], w1);
+            if (q + 1 < QB) {
+              w = cmul(w, st);
+              w1 = cmul(w1, st1);
+            }
+          }
+        } else {
+#pragma unroll
+          for (int q = 0; q < QB; ++q) {
+            x[dl * QB + q] = cmul(x[dl * QB + q], w);
+            y[dl * QB + q] = cmul(y[dl * QB + q], w);
+            if (q + 1 < QB) w = cmul(w, st);
+          }
+        }
+      }
+#pragma unroll
+      for (int dl = 0; dl < DB; ++dl) {
+        reg_dft<float, QB>(x + dl * QB);
+        reg_dft<float, QB>(y + dl * QB);
+      }
+      {  // W_RB^(p kq)
+        const V* wp = w256;
+#pragma unroll
+        for (int k = 1; k < QB; ++k) {
+          wp += r * (256 / RB);
+          const V w = *wp;
+#pragma unroll
+          for (int dl = 0; dl < DB; ++dl) {
+            x[dl * QB + P<QB>(k)] = cmul(x[dl * QB + P<QB>(k)], w);
+            y[dl * QB + P<QB>(k)] = cmul(y[dl * QB + P<QB>(k)], w);
+          }
+        }
+      }
+      // consumed staging lines: 8 threads share a line, thread cp drops the
+      // lines of its loads cp and cp + 8
+#pragma unroll
+      for (int i = cp; i < 16; i += 8) l2_discard(sp + pair_b_line<RB, T1>(task, i / QB, r, i % QB));
+#pragma unroll
+      for (int dl = 0; dl < DB; ++dl)
+#pragma unroll
+        for (int k = 0; k < QB; ++k) {
+          const V u = x[dl * QB + P<QB>(k)], w = y[dl * QB + P<QB>(k)];
+          xq[((dl * QB + k) * 16 + r) * 8 + cp] = make_float4(u.x, u.y, w.x, w.y);
+        }
+    } else {
+      // ---- A stage 0: 16-point DFTs over t, W_256^(s kt) shared by the pair
+      if (a.check_finite) {
+#pragma unroll
+        for (int t = 0; t < 16; ++t)
+          nf |= !(isfinite(x[t].x) && isfinite(x[t].y) && isfinite(y[t].x) && isfinite(y[t].y));
+      }
+      if constexpr (T1) {
+        const V ci = cvt(a.cin, 0.f);
+#pragma unroll
+        for (int t = 0; t < 16; ++t) {
+          x[t] = mul2(x[t], ci);
+          y[t] = mul2(y[t], ci);
+        }
+      }
+      reg_dft<float, 16>(x);
+      reg_dft<float, 16>(y);
+      {
+        const V* wp = w256;
+#pragma unroll
+        for (int k = 1; k < 16; ++k) {
+          wp += r;
+          const V w = *wp;
+          x[P<16>(k)] = cmul(x[P<16>(k)], w);
+          y[P<16>(k)] = cmul(y[P<16>(k)], w);
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < 16; ++k) {
+        if constexpr (T1) {  // [s][kt][j2]: s pitch 273, kt pitch 17
+          xb[r * 273 + k * 17 + 2 * cp] = x[P<16>(k)];
+          xb[r * 273 + k * 17 + 2 * cp + 1] = y[P<16>(k)];
+        } else {  // [kt][s][pair]
+          const V u = x[P<16>(k)], w = y[P<16>(k)];
+          xq[(k * 16 + r) * 8 + cp] = make_float4(u.x, u.y, w.x, w.y);
+        }
+      }
+    }
+    sc.before_exchange(a, g);
+    __syncthreads();
+    if (isB) {
+      // ---- B stage 1: 16-point DFTs over p; thread (cp, dl, kq)
+      const int kq = r % QB, dl = r / QB;
+#pragma unroll
+      for (int u = 0; u < 16; ++u) {
+        const float4 t = xq[((dl * QB + kq) * 16 + u) * 8 + cp];
+        x[u] = make_float2(t.x, t.y);
+        y[u] = make_float2(t.z, t.w);
+      }
+      reg_dft<float, 16>(x);
+      reg_dft<float, 16>(y);
+      const uint64_t pol = policy_evict_first();
+      if constexpr (T1) {
+        // y[k1 + R1 j2] = Y W_N^(j2 k1), k1 = kt + 16 ks + 256 kq + 256 QB kp, kt = 2cp (+1)
+        const int j2 = g * 16 + (task >> 4) * DB + dl;
+        const uint32_t c = (uint32_t)(2 * cp + 16 * (task & 15) + 256 * kq);
+        V w = w_full(T4, (uint32_t)((uint64_t)j2 * c));
+        const V w1 = w_full(T4, (uint32_t)j2);  // W_N^j2: column kt + 1
+        const V st = w_full(T4, (uint32_t)(((uint64_t)j2 * (256 * QB)) % (uint64_t)a.N));
+        V* op = DST + (int64_t)j2 * a.R + c;
+#pragma unroll
+        for (int kp = 0; kp < 16; ++kp) {
+          pair::st16(op + kp * (256 * QB), cmul(x[P<16>(kp)], w), cmul(y[P<16>(kp)], cmul(w, w1)), pol);
+          if (kp < 15) w = cmul(w, st);
+        }
+      } else {
+        const int kb = task * DB + dl;
+        const V co = cvt(a.cout, 0.f);
+        V* op = DST + (int64_t)g * 16 + 2 * cp + a.LS * (int64_t)(kb + 256 * kq);
+        const int64_t step = a.LS * (int64_t)(256 * QB);
+#pragma unroll
+        for (int kp = 0; kp < 16; ++kp) pair::st16(op + kp * step, mul2(x[P<16>(kp)], co), mul2(y[P<16>(kp)], co), pol);
+      }
+    } else {
+      // ---- A stage 1: 16-point DFTs over s -> ks, store to the ring
+      // T0 thread (pair cp, kt = r): ring [kb][ja][lane], kb = kt + 16 ks
+      // T1 thread (kt pair cp, j2l = r): ring [j2l][ja][ks][kt]
+#pragma unroll
+      for (int u = 0; u < 16; ++u) {
+        if constexpr (T1) {
+          x[u] = xb[u * 273 + (2 * cp) * 17 + r];
+          y[u] = xb[u * 273 + (2 * cp + 1) * 17 + r];
+        } else {
+          const float4 t = xq[(r * 16 + u) * 8 + cp];
+          x[u] = make_float2(t.x, t.y);
+          y[u] = make_float2(t.z, t.w);
+        }
+      }
+      reg_dft<float, 16>(x);
+      reg_dft<float, 16>(y);
+      const int base = T1 ? (r * RB + task) * 256 + 2 * cp : (r * RB + task) * 16 + 2 * cp;
+      const int step = T1 ? 16 : 16 * RB * 16;
+      const uint64_t keep = policy_evict_last();
+#pragma unroll
+      for (int ks = 0; ks < 16; ++ks) pair::st16(sp + base + ks * step, x[P<16>(ks)], y[P<16>(ks)], keep);
+    }
+    sc.end(a, isB, g);
+  }
+  sc.finish(a, nf);
 #undef SRC
 #undef DST
 #undef STG
@@ -414,6 +715,19 @@ template <typename R>
 static void* pick(int ra, int rb, bool t1) {
   return ra == 192 ? pick_ra<R, 192>(rb, t1) : pick_ra<R, 256>(rb, t1);
 }
+static void* pick_pair(int rb, bool t1) {
+  switch (rb) {
+    case 32: return t1 ? (void*)lean_pair<32, true> : (void*)lean_pair<32, false>;
+    case 64: return t1 ? (void*)lean_pair<64, true> : (void*)lean_pair<64, false>;
+    case 128: return t1 ? (void*)lean_pair<128, true> : (void*)lean_pair<128, false>;
+    case 256: return t1 ? (void*)lean_pair<256, true> : (void*)lean_pair<256, false>;
+    default: return nullptr;
+  }
+}
+static bool use_pair() {
+  static const int v = getenv("EFFT_LEAN_PAIR") ? atoi(getenv("EFFT_LEAN_PAIR")) : 1;
+  return v != 0;
+}
 
 bool plan(int64_t n, int c128, int inverse, bool scale_inverse, bool check_finite, int num_sms, Pass p[2],
           int64_t* staging_elems, int* err_cuda) {
@@ -441,10 +755,12 @@ bool plan(int64_t n, int c128, int inverse, bool scale_inverse, bool check_finit
     const int64_t R = t1 ? R1 : R2;
     q.ra = t1 ? ra1 : 256;
     q.rb = 1 << (t1 ? lb1 : lb2);
-    q.fn = reinterpret_cast<void (*)(Args)>(c128 ? pick<double>(q.ra, q.rb, t1) : pick<float>(q.ra, q.rb, t1));
+    const bool paired = !c128 && q.ra == 256 && use_pair();
+    q.fn = reinterpret_cast<void (*)(Args)>(paired ? pick_pair(q.rb, t1)
+                                            : c128 ? pick<double>(q.ra, q.rb, t1) : pick<float>(q.ra, q.rb, t1));
     if (!q.fn) return false;
-    q.nt = NT;
-    q.smem = (int)((256 * (F + 1) + (q.ra == 256 ? 2 : 4) * 256) * elem);
+    q.nt = paired ? pair::NT : NT;
+    q.smem = paired ? (int)((pair::XB2 + 512) * elem) : (int)((256 * (F + 1) + (q.ra == 256 ? 2 : 4) * 256) * elem);
     Args& a = q.a;
     a = Args{};
     a.R = R;
@@ -464,7 +780,8 @@ bool plan(int64_t n, int c128, int inverse, bool scale_inverse, bool check_finit
       return false;
     }
     int occ = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void*)q.fn, NT, q.smem) != cudaSuccess || occ < 1) {
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void*)q.fn, q.nt, q.smem) != cudaSuccess ||
+        occ < 1) {
       *err_cuda = 1;
       return false;
     }
