@@ -364,6 +364,14 @@ def run_ours(args):
     dom = max(range(len(avg)), key=lambda k: avg[k])
     alg_bytes = 2 * n * ELEM[dtype]
     achieved = alg_bytes / (avg[dom] * 1e-3) / 1e9
+    traffic = None  # DRAM bytes per launch of that kernel from the committed ncu capture
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as fh:
+            tr = json.load(fh).get(args.config)
+        if tr:
+            traffic = tr["pass_bytes"][dom]
+    except (OSError, ValueError, KeyError, IndexError):
+        traffic = None
     whole_gbs = per_step * fwd.launches() * alg_bytes / (ms_per_step * 1e-3) / 1e9
 
     # e2e through the C-ABI host-buffer entry (rank-local), fewer steps: PCIe bound
@@ -416,7 +424,7 @@ def run_ours(args):
                        "plan": fwd.describe().strip().splitlines()},
             "hbm_gbs_whole_step": round(whole_gbs, 1),
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
-                         "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": None,
+                         "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": traffic,
                          "kernel": f"pass {dom} of {len(avg)} (lean_pass kernel), {avg[dom]:.4f} ms avg",
                          "pass_ms": [round(a, 4) for a in avg], "peak_source": peak_src,
                          "alg_bytes_per_launch": alg_bytes},

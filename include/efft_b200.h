@@ -81,9 +81,14 @@ int efft_plan_launches(efft_plan_t plan, int *launches);
 int efft_execute(efft_plan_t plan, const void *d_in, void *d_out, void *stream);
 
 /* End-to-end call with HOST buffers (pinned or pageable): copies h_in to a
- * plan-owned device input, runs efft_execute, copies the result to h_out and
- * synchronises the stream. */
+ * device input, runs efft_execute, copies the result to h_out and
+ * synchronises the stream.  The device in/out pair is one per-device pool
+ * shared by all plans (grown on demand, serialised by a lock), so a forward
+ * and an inverse plan of the same size need one pair between them. */
 int efft_execute_host(efft_plan_t plan, const void *h_in, void *h_out, void *stream);
+
+/* Frees the per-device pool of efft_execute_host (it is re-created on demand). */
+int efft_release_host_buffers(int device);
 
 /* Returns (synchronising) whether any non-finite input value was seen by
  * executions since the last call, and clears the flag. */

@@ -42,6 +42,7 @@ EXPORTED = (
     "efft_plan_launches",
     "efft_execute",
     "efft_execute_host",
+    "efft_release_host_buffers",
     "efft_nonfinite_seen",
     "efft_plan_destroy",
     "efft_plan_enable_timing",
@@ -76,6 +77,7 @@ def load():
     lib.efft_plan_launches.argtypes = [vp, ctypes.POINTER(i32)]
     lib.efft_execute.argtypes = [vp, vp, vp, vp]
     lib.efft_execute_host.argtypes = [vp, vp, vp, vp]
+    lib.efft_release_host_buffers.argtypes = [i32]
     lib.efft_nonfinite_seen.argtypes = [vp, ctypes.POINTER(i32), vp]
     lib.efft_plan_destroy.argtypes = [vp]
     lib.efft_plan_enable_timing.argtypes = [vp, i32]
@@ -99,6 +101,10 @@ def check(rc: int, what: str = "") -> None:
     msg = load().efft_last_error().decode(errors="replace")
     exc = _STATUS.get(rc, errors.DeviceError)
     raise exc(f"{what}: {msg}" if what else msg)
+
+
+def release_host_buffers(device: int = 0) -> None:
+    check(load().efft_release_host_buffers(device), "efft_release_host_buffers")
 
 
 def permute_swap01(d_in: int, d_out: int, n0: int, n1: int, n2: int, elem: int, stream: int) -> None:

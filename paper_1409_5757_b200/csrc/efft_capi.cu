@@ -19,6 +19,7 @@
 #include <cstdlib>
 #include <algorithm>
 #include <cstring>
+#include <mutex>
 #include <string>
 
 #include "../../include/efft_b200.h"
@@ -69,6 +70,19 @@ __global__ void real_split_kernel(float2* z, int64_t h, int64_t n) {
 
 thread_local std::string g_err;
 
+// Device in/out pair of efft_execute_host, one per device, shared by all plans.
+constexpr int kMaxDevices = 64;
+struct HostPool {
+  std::mutex mu;
+  void* in = nullptr;
+  void* out = nullptr;
+  size_t bytes = 0;
+};
+HostPool& host_pool(int device) {
+  static HostPool pools[kMaxDevices];
+  return pools[device];
+}
+
 int fail(int code, const char* fmt, ...) {
   char buf[512];
   va_list ap;
@@ -115,8 +129,6 @@ struct efft_plan_s {
   int32_t* counters = nullptr;
   size_t counter_bytes = 0;
   int32_t* flag = nullptr;
-  void* h_dev_in = nullptr;  // lazily allocated for efft_execute_host
-  void* h_dev_out = nullptr;
   int num_sms = 0;
   bool timing = false;
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};  // launch boundaries
@@ -770,7 +782,34 @@ int efft_execute(efft_plan_t pl, const void* d_in, void* d_out, void* stream) {
     efft::lean::Args a = q.a;
     a.src = p == 0 ? d_in : d_out;
     a.dst = d_out;
-    q.fn<<<q.grid, q.nt, q.smem, s>>>(a);
+    static const int persist = env_int("EFFT_L2_PERSIST", 0);
+    if (persist) {
+      // experimental: keep the staging ring L2-resident (persisting window)
+      static bool limit_set = false;
+      if (!limit_set) {
+        cudaDeviceProp prop;
+        cudaGetDeviceProperties(&prop, pl->device);
+        cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, (size_t)prop.persistingL2CacheMaxSize);
+        limit_set = true;
+      }
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(q.grid);
+      cfg.blockDim = dim3(q.nt);
+      cfg.dynamicSmemBytes = q.smem;
+      cfg.stream = s;
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeAccessPolicyWindow;
+      at[0].val.accessPolicyWindow.base_ptr = pl->staging;
+      at[0].val.accessPolicyWindow.num_bytes = pl->staging_bytes;
+      at[0].val.accessPolicyWindow.hitRatio = 1.0f;
+      at[0].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+      at[0].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+      cfg.attrs = at;
+      cfg.numAttrs = 1;
+      CUDA_TRY(cudaLaunchKernelEx(&cfg, q.fn, a));
+    } else {
+      q.fn<<<q.grid, q.nt, q.smem, s>>>(a);
+    }
     CUDA_TRY(cudaGetLastError());
   }
   for (int p = 0; !pl->lean && p < pl->npass; ++p) {
@@ -801,18 +840,43 @@ int efft_execute_host(efft_plan_t pl, const void* h_in, void* h_out, void* strea
   if (!pl || !h_in || !h_out) return fail(EFFT_ERR_INVALID_ARG, "NULL argument");
   CUDA_TRY(cudaSetDevice(pl->device));
   const size_t bytes = (size_t)pl->n * pl->elem;
-  if (!pl->h_dev_in) {
-    if (cudaMalloc(&pl->h_dev_in, bytes) != cudaSuccess || cudaMalloc(&pl->h_dev_out, bytes) != cudaSuccess) {
+  // The device in/out pair is shared by every plan of the device (one pool,
+  // grown on demand), so a forward and an inverse plan of a 64 GiB transform
+  // need 128 GiB between them, not 256.  The call is synchronous and holds the
+  // pool's lock until its copies are done.
+  HostPool& hp = host_pool(pl->device);
+  std::lock_guard<std::mutex> lock(hp.mu);
+  if (hp.bytes < bytes) {
+    if (hp.in) cudaFree(hp.in);
+    if (hp.out) cudaFree(hp.out);
+    hp.in = hp.out = nullptr;
+    hp.bytes = 0;
+    if (cudaMalloc(&hp.in, bytes) != cudaSuccess || cudaMalloc(&hp.out, bytes) != cudaSuccess) {
       cudaGetLastError();
+      if (hp.in) cudaFree(hp.in);
+      hp.in = nullptr;
       return fail(EFFT_ERR_ALLOC, "device buffers for host execution (%zu bytes each)", bytes);
     }
+    hp.bytes = bytes;
   }
   cudaStream_t s = (cudaStream_t)stream;
-  CUDA_TRY(cudaMemcpyAsync(pl->h_dev_in, h_in, bytes, cudaMemcpyHostToDevice, s));
-  int rc = efft_execute(pl, pl->h_dev_in, pl->h_dev_out, stream);
+  CUDA_TRY(cudaMemcpyAsync(hp.in, h_in, bytes, cudaMemcpyHostToDevice, s));
+  int rc = efft_execute(pl, hp.in, hp.out, stream);
   if (rc != EFFT_OK) return rc;
-  CUDA_TRY(cudaMemcpyAsync(h_out, pl->h_dev_out, bytes, cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(cudaMemcpyAsync(h_out, hp.out, bytes, cudaMemcpyDeviceToHost, s));
   CUDA_TRY(cudaStreamSynchronize(s));
+  return EFFT_OK;
+}
+
+int efft_release_host_buffers(int device) {
+  if (device < 0 || device >= kMaxDevices) return fail(EFFT_ERR_INVALID_ARG, "device %d", device);
+  HostPool& hp = host_pool(device);
+  std::lock_guard<std::mutex> lock(hp.mu);
+  CUDA_TRY(cudaSetDevice(device));
+  if (hp.in) cudaFree(hp.in);
+  if (hp.out) cudaFree(hp.out);
+  hp.in = hp.out = nullptr;
+  hp.bytes = 0;
   return EFFT_OK;
 }
 
@@ -856,8 +920,6 @@ int efft_plan_destroy(efft_plan_t pl) {
   if (pl->counters) cudaFree(pl->counters);
   if (pl->flag) cudaFree(pl->flag);
   if (pl->lean_t4) cudaFree(pl->lean_t4);
-  if (pl->h_dev_in) cudaFree(pl->h_dev_in);
-  if (pl->h_dev_out) cudaFree(pl->h_dev_out);
   delete pl;
   return EFFT_OK;
 }

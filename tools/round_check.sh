@@ -11,6 +11,6 @@ python bench.py --steps 2 --warmup 3 --no-cpu --no-e2e > gpurun_out/bench_small.
 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches.csv \
     python bench.py --steps 2 --warmup 3 --no-cpu --no-e2e > gpurun_out/ncu_launch.log 2>&1
 python tools/prof_run.py c3 1 > gpurun_out/plain.log 2>&1 && \
-ncu --set full --clock-control none --import-source on -k regex:lean_pass -c 2 -o gpurun_out/lean_c3 \
+ncu --set full --clock-control none --import-source on -k regex:lean -c 2 -o gpurun_out/lean_c3 \
     python tools/prof_run.py c3 1 > gpurun_out/ncu_full.log 2>&1
 echo done
