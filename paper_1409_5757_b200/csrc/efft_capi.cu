@@ -782,34 +782,7 @@ int efft_execute(efft_plan_t pl, const void* d_in, void* d_out, void* stream) {
     efft::lean::Args a = q.a;
     a.src = p == 0 ? d_in : d_out;
     a.dst = d_out;
-    static const int persist = env_int("EFFT_L2_PERSIST", 0);
-    if (persist) {
-      // experimental: keep the staging ring L2-resident (persisting window)
-      static bool limit_set = false;
-      if (!limit_set) {
-        cudaDeviceProp prop;
-        cudaGetDeviceProperties(&prop, pl->device);
-        cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, (size_t)prop.persistingL2CacheMaxSize);
-        limit_set = true;
-      }
-      cudaLaunchConfig_t cfg = {};
-      cfg.gridDim = dim3(q.grid);
-      cfg.blockDim = dim3(q.nt);
-      cfg.dynamicSmemBytes = q.smem;
-      cfg.stream = s;
-      cudaLaunchAttribute at[1];
-      at[0].id = cudaLaunchAttributeAccessPolicyWindow;
-      at[0].val.accessPolicyWindow.base_ptr = pl->staging;
-      at[0].val.accessPolicyWindow.num_bytes = pl->staging_bytes;
-      at[0].val.accessPolicyWindow.hitRatio = 1.0f;
-      at[0].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
-      at[0].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
-      cfg.attrs = at;
-      cfg.numAttrs = 1;
-      CUDA_TRY(cudaLaunchKernelEx(&cfg, q.fn, a));
-    } else {
-      q.fn<<<q.grid, q.nt, q.smem, s>>>(a);
-    }
+    q.fn<<<q.grid, q.nt, q.smem, s>>>(a);
     CUDA_TRY(cudaGetLastError());
   }
   for (int p = 0; !pl->lean && p < pl->npass; ++p) {

@@ -792,7 +792,7 @@ bool plan(int64_t n, int c128, int inverse, bool scale_inverse, bool check_finit
     const int64_t window = (4 * (int64_t)q.grid + per - 1) / per;
     int64_t lag = window + 1;
     if (const char* ev = getenv("EFFT_LEAN_LAG")) lag = atoi(ev);
-    int64_t slots = lag + window + 2;
+    int64_t slots = lag + (window + 1) / 2 + 2;
     if (const char* ev = getenv("EFFT_LEAN_SLOTS")) slots = atoi(ev);
     if (lag < 1) lag = 1;
     if (lag > a.ngroups) lag = a.ngroups;
