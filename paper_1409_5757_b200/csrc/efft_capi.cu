@@ -162,17 +162,12 @@ int env_int(const char* name, int dflt) {
 }
 
 bool get_staged(int dtype, int ra, int rb, KernelInfo* k) {
-  // EFFT_WS=1/0 forces the warp-specialised TMA kernel / the register-path
-  // kernel; default: TMA kernel for complex64, register path for complex128
-  // (the faster measured variant of each)
-  const int ws = env_int("EFFT_WS", dtype == EFFT_C64 ? 1 : 0);
-  return dtype == EFFT_C64 ? efft::get_staged_kernel_f32(ra, rb, ws, k)
-                           : efft::get_staged_kernel_f64(ra, rb, ws, k);
+  return dtype == EFFT_C64 ? efft::get_staged_kernel_f32(ra, rb, k) : efft::get_staged_kernel_f64(ra, rb, k);
 }
 
 
 // Decide direct vs staged and the sub-radices of one pass of radix R.
-bool pick_pass(int dtype, int64_t R, PassPlan* pp, int64_t ncols = 0) {
+bool pick_pass(int dtype, int64_t R, PassPlan* pp) {
   pp->radix = R;
   const bool has3 = (R % 3) == 0;
   const int64_t dmax = has3 ? 384 : 512;
@@ -180,35 +175,14 @@ bool pick_pass(int dtype, int64_t R, PassPlan* pp, int64_t ncols = 0) {
     pp->staged = false;
     pp->rho_a = R;
     pp->rho_b = 0;
-    // TMA-prefetching direct tiles when every tile is full (EFFT_DIRECT_TP=1)
-    static const int dtp = env_int("EFFT_DIRECT_TP", 0);
-    if (dtp && dtype == EFFT_C64 && !has3 && R >= 16 && ncols > 0 && efft::get_direct_tp_f32((int)R, &pp->k) &&
-        ncols % (pp->k.d_a * 16) == 0)
-      return true;
     return get_direct(dtype, (int)R, &pp->k);
   }
   pp->staged = true;
   pp->rho_a = has3 ? 384 : 256;
   pp->rho_b = R / pp->rho_a;
   if (pp->rho_b * pp->rho_a != R || pp->rho_b > 512) return false;
-  // complex64 power-of-two passes: EFFT_C64_TILE=256 selects 32 KB tiles (4 CTAs/SM)
-  static const int c64_tile = env_int("EFFT_C64_TILE", 512);
-  const int ws = env_int("EFFT_WS", dtype == EFFT_C64 ? 1 : 0);
   bool ok;
-  if (dtype == EFFT_C64 && !has3 && c64_tile == 256 && !ws && pp->rho_b <= 256)
-    ok = efft::get_staged_small_f32((int)pp->rho_b, &pp->k);
-  else if (dtype == EFFT_C64 && !has3 && c64_tile == 1 && !ws && pp->rho_b >= 8 && pp->rho_b <= 256)
-    ok = efft::get_staged_wide_f32((int)pp->rho_b, &pp->k);
-  else if (dtype == EFFT_C64 && !has3 && c64_tile == 4 && pp->rho_b >= 8 && pp->rho_b <= 256)
-    ok = efft::get_staged_ws32_f32((int)pp->rho_b, &pp->k);
-  else if (!has3 && c64_tile == 3 && !ws && pp->rho_b >= 8 && pp->rho_b <= 256)
-    ok = dtype == EFFT_C64 ? efft::get_staged_tp_f32((int)pp->rho_b, &pp->k)
-                           : efft::get_staged_tp_f64((int)pp->rho_b, &pp->k);
-  else if (!has3 && c64_tile == 2 && !ws && pp->rho_b >= 8 && pp->rho_b <= 256)
-    ok = dtype == EFFT_C64 ? efft::get_staged_pf_f32((int)pp->rho_b, &pp->k)
-                           : efft::get_staged_pf_f64((int)pp->rho_b, &pp->k);
-  else
-    ok = get_staged(dtype, (int)pp->rho_a, (int)pp->rho_b, &pp->k);
+  ok = get_staged(dtype, (int)pp->rho_a, (int)pp->rho_b, &pp->k);
   if (!ok) return false;
   // A tiles take D_A = tpts/rho_a consecutive u (D_A | rho_b); B tiles cover
   // D_B = tpts/rho_b outputs k1 of the rho_a-point DFTs (D_B | rho_a)
@@ -481,7 +455,7 @@ int build_plan(efft_plan_s* pl) {
   size_t staging_bytes = 0;
   for (int p = 0; p < pl->npass; ++p) {
     PassPlan& pp = pl->pass[p];
-    if (!pick_pass(dt, radices[p], &pp, pl->n / radices[p]))
+    if (!pick_pass(dt, radices[p], &pp))
       return fail(EFFT_ERR_UNSUPPORTED_SIZE, "no kernel for radix %lld", (long long)radices[p]);
     describe_pass(pl, p, pl->npass, radices[p], pl->columns ? pl->col_count : ns);
     if (pl->columns) {  // column store (Ns = cols), caller-chosen twiddle, unscaled inverse

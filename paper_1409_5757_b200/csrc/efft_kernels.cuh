@@ -1255,317 +1255,6 @@ __global__ void __launch_bounds__(TA::NT + 32, (TA::TILE * (int)sizeof(typename 
   }
 }
 
-// Software-pipelined persistent staged pass (register double buffering).
-// Each CTA claims task k+1 while it works on task k and, if k+1's dependency
-// is already satisfied (non-blocking check), issues k+1's global loads into a
-// second register set BEFORE computing task k, so the DRAM / L2 latency of the
-// next tile hides behind the current tile's DFT work.  If the dependency is
-// not ready yet the load is deferred until task k is done (a blocking wait is
-// then deadlock-free: every wait targets an earlier task and this CTA holds
-// no unfinished task).
-template <typename R, class TA, class TB>
-__global__ void __launch_bounds__(TA::NT, 1) pf_kernel(const __grid_constant__ PassArgs p) {
-  using V = typename CT<R>::V;
-  static_assert(TA::E == TB::E && TA::NT == TB::NT, "A and B tiles share the register footprint");
-  constexpr int E = TA::E;
-  extern __shared__ __align__(128) unsigned char smem_raw[];
-  constexpr int SM_ELEMS = TA::SMEM_ELEMS > TB::SMEM_ELEMS ? TA::SMEM_ELEMS : TB::SMEM_ELEMS;
-  V* sm = reinterpret_cast<V*>(smem_raw);
-  V* twA = sm + SM_ELEMS;
-  V* twB = twA + TA::RHO;
-  __shared__ long long s_pos[2], s_grp[2];
-  __shared__ int s_sub[2], s_slot[2], s_isB[2], s_ready[2];
-  TA::build_table(twA);
-  TB::build_table(twB);
-  const int64_t G = p.ngroups;
-  (void)G;
-  auto publish = [&](int b, unsigned long long pos) {  // thread 0
-    s_pos[b] = (long long)pos;
-    if ((int64_t)pos >= p.total_tasks) return;
-    bool isB;
-    int64_t grp, sub;
-    decode_task(p, (int64_t)pos, isB, grp, sub);
-    s_isB[b] = isB;
-    s_grp[b] = grp;
-    s_sub[b] = (int)sub;
-    s_slot[b] = (int)(grp % p.nslots);
-    const int32_t* ctr = isB ? p.doneA + grp : (grp >= p.nslots ? p.doneB + (grp - p.nslots) : nullptr);
-    const int32_t need = isB ? p.a.ntasks : p.b.ntasks;
-    const bool ok = ctr == nullptr || *(volatile const int32_t*)ctr >= need;
-    if (ok) __threadfence();
-    s_ready[b] = ok;
-  };
-  auto wait_dep = [&](int b) {  // all threads; blocking
-    if (threadIdx.x == 0) {
-      const int64_t grp = s_grp[b];
-      const bool isB = s_isB[b];
-      const int32_t* ctr = isB ? p.doneA + grp : (grp >= p.nslots ? p.doneB + (grp - p.nslots) : nullptr);
-      const int32_t need = isB ? p.a.ntasks : p.b.ntasks;
-      if (ctr != nullptr) {
-        while (*(volatile const int32_t*)ctr < need) __nanosleep(64);
-        __threadfence();
-      }
-    }
-    __syncthreads();
-  };
-  auto load_task = [&](int b, V* v, bool& nf) {
-    const int64_t grp = s_grp[b];
-    const int sub = s_sub[b], slot = s_slot[b];
-    if (s_isB[b])
-      TB::load_any(p.b, TB::source(p.b, p, grp, sub, slot), grp, v, nf);
-    else
-      TA::load_any(p.a, TA::source(p.a, p, grp, sub, slot), grp, v, nf);
-  };
-  bool nonfinite = false;
-  V cur[E], nxt[E];
-  if (threadIdx.x == 0) publish(0, atomicAdd(p.task_counter, 1ull));
-  __syncthreads();
-  if (s_pos[0] >= p.total_tasks) return;
-  wait_dep(0);
-  load_task(0, cur, nonfinite);
-  int b = 0;
-  for (;;) {
-    // claim and decode the next task; prefetch its tile if its producers are done
-    if (threadIdx.x == 0) publish(b ^ 1, atomicAdd(p.task_counter, 1ull));
-    __syncthreads();
-    const bool has_next = s_pos[b ^ 1] < p.total_tasks;
-    const bool early = has_next && s_ready[b ^ 1];
-    if (early) load_task(b ^ 1, nxt, nonfinite);
-    // process the current task
-    {
-      const int64_t grp = s_grp[b];
-      const int sub = s_sub[b], slot = s_slot[b];
-      if (!s_isB[b]) {
-        TA::process(p.a, p, grp, sub, slot, cur, sm, twA, nullptr, nullptr);
-        __syncthreads();
-        if (threadIdx.x == 0) {
-          __threadfence();
-          atomicAdd(p.doneA + grp, 1);
-        }
-      } else {
-        TB::process(p.b, p, grp, sub, slot, cur, sm, twB, p.doneB + grp, TB::source(p.b, p, grp, sub, slot));
-      }
-      __syncthreads();
-    }
-    if (!has_next) break;
-    if (!early) {
-      wait_dep(b ^ 1);
-      load_task(b ^ 1, nxt, nonfinite);
-    }
-#pragma unroll
-    for (int i = 0; i < E; ++i) cur[i] = nxt[i];
-    b ^= 1;
-  }
-  if (__syncthreads_or(nonfinite) && threadIdx.x == 0) atomicOr(p.flag, 1);
-}
-
-// TMA-prefetching persistent staged pass, static schedule.
-// CTA c owns task positions c, c + G, c + 2G, ... of the staged order
-// (decode_task).  Thread 0 keeps NBUF-1 tiles in flight: between tiles it
-// decodes the next position (32-bit integer math), checks the tile's
-// producer counter from a load it issued one tile earlier (so no global
-// round trip sits on the critical path), and issues ONE TMA tensor copy
-// (HBM input for A tiles, the L2 staging ring for B tiles) into the buffer
-// freed by the previous tile.  A tile whose producers were not done is
-// copied just before it is needed (blocking wait; deadlock-free because the
-// smallest unfinished task is always owned by a CTA that has finished all its
-// earlier tasks).  Completion counters are bumped with release reductions.
-
-template <typename R, class TA, class TB, int NBUF>
-__global__ void __launch_bounds__(TA::NT, 1) tp_kernel(const __grid_constant__ PassArgs p) {
-  using V = typename CT<R>::V;
-  static_assert(TA::NT == TB::NT && TA::TOFF == 0 && TB::TOFF == 0, "all threads compute");
-  static_assert(TA::SWZ && TB::SWZ, "TMA tiles land 128B-swizzled");
-  extern __shared__ __align__(128) unsigned char smem_raw[];
-  constexpr int BUF = TA::SMEM_ELEMS > TB::SMEM_ELEMS ? TA::SMEM_ELEMS : TB::SMEM_ELEMS;
-  static_assert((BUF * sizeof(V)) % 1024 == 0, "swizzled buffers stay 1024-byte aligned");
-  V* bufs = reinterpret_cast<V*>(smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u));
-  V* twA = bufs + NBUF * BUF;
-  V* twB = twA + TA::RHO;
-  __shared__ __align__(8) uint64_t full[NBUF];
-  __shared__ int t_grp[NBUF], t_sub[NBUF], t_slot[NBUF], t_isB[NBUF], t_issued[NBUF];
-  if (threadIdx.x == 0)
-    for (int i = 0; i < NBUF; ++i) mbar_init(&full[i], 1);
-  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  TA::build_table(twA);
-  TB::build_table(twB);
-  const uint64_t pol = policy_evict_first();
-  const uint32_t T = (uint32_t)p.total_tasks, G = gridDim.x;
-  const uint32_t NG = (uint32_t)p.ngroups, LAG = (uint32_t)p.lag, TAn = (uint32_t)p.a.ntasks,
-                 TBn = (uint32_t)p.b.ntasks, NS = (uint32_t)p.nslots;
-  // ---- thread-0 producer state
-  int32_t pre_val = 0;        // prefetched producer-counter value for the next claim
-  const int32_t* pre_ctr = nullptr;
-  uint32_t next_k = 0;        // local index of the next task to claim
-  auto decode32 = [&](uint32_t pos, bool& isB, uint32_t& grp, uint32_t& sub) {
-    if (pos < LAG * TAn) {
-      isB = false;
-      grp = pos / TAn;
-      sub = pos % TAn;
-    } else if (pos < LAG * TAn + (NG - LAG) * (TAn + TBn)) {
-      const uint32_t q = pos - LAG * TAn;
-      const uint32_t i = LAG + q / (TAn + TBn), r = q % (TAn + TBn);
-      isB = r < TBn;
-      grp = isB ? i - LAG : i;
-      sub = isB ? r : r - TBn;
-    } else {
-      const uint32_t q = pos - LAG * TAn - (NG - LAG) * (TAn + TBn);
-      isB = true;
-      grp = NG - LAG + q / TBn;
-      sub = q % TBn;
-    }
-  };
-  auto ctr_of = [&](bool isB, uint32_t grp) -> const int32_t* {
-    return isB ? p.doneA + grp : (grp >= NS ? p.doneB + (grp - NS) : nullptr);
-  };
-  auto issue = [&](int b) {
-    V* dst = bufs + b * BUF;
-    const int grp = t_grp[b], sub = t_sub[b];
-    if (!t_isB[b]) {
-      constexpr int W = (int)sizeof(V) / 8;
-      constexpr int BOX = TA::RHO > 256 ? TA::RHO / 2 : TA::RHO;
-      mbar_arrive_tx(&full[b], (uint32_t)(TA::D * TA::RHO * 128));
-#pragma unroll
-      for (int h = 0; h < TA::RHO / BOX; ++h)
-        tma_load_3d(dst + h * BOX * TA::D * TA::F, &p.tmA, grp * TA::F * W, sub * TA::D, h * BOX, &full[b], pol);
-    } else {
-      constexpr int BOX = TB::RHO > 256 ? TB::RHO / 2 : TB::RHO;
-      mbar_arrive_tx(&full[b], (uint32_t)(TB::D * TB::RHO * 128));
-#pragma unroll
-      for (int h = 0; h < TB::RHO / BOX; ++h)
-        tma_load_4d(dst + h * BOX * TB::D * TB::F, &p.tmB, 0, sub * TB::D, h * BOX, t_slot[b], &full[b], pol);
-    }
-    t_issued[b] = 1;
-  };
-  // claim local task next_k into buffer b: decode, test the prefetched counter,
-  // issue the copy if ready, then prefetch the counter of the following task
-  auto claim = [&](int b) {
-    const uint32_t pos = blockIdx.x + next_k * G;
-    ++next_k;
-    t_issued[b] = 0;
-    t_grp[b] = -1;
-    if (pos >= T) return;
-    bool isB;
-    uint32_t grp, sub;
-    decode32(pos, isB, grp, sub);
-    t_isB[b] = isB;
-    t_grp[b] = (int)grp;
-    t_sub[b] = (int)sub;
-    t_slot[b] = (int)(grp % NS);
-    const int32_t need = isB ? (int32_t)TAn : (int32_t)TBn;
-    const int32_t* ctr = ctr_of(isB, grp);
-    // pre_val came from an acquire load issued one tile ago: if it already
-    // covers `need`, the producers' stores happen-before this copy
-    bool ready = ctr == nullptr || (ctr == pre_ctr && pre_val >= need);
-    if (!ready && ctr != nullptr) ready = ld_acquire(ctr) >= need;  // rare slow path
-    if (ready) {
-      if (ctr != nullptr) fence_proxy_async();
-      issue(b);
-    }
-    // prefetch the producer counter of the next claim (consumed one tile later)
-    const uint32_t npos = blockIdx.x + next_k * G;
-    pre_ctr = nullptr;
-    if (npos < T) {
-      bool nb;
-      uint32_t ng, ns;
-      decode32(npos, nb, ng, ns);
-      pre_ctr = ctr_of(nb, ng);
-      if (pre_ctr != nullptr) pre_val = ld_acquire(pre_ctr);
-    }
-  };
-  if (threadIdx.x == 0) {
-    const uint32_t pos0 = blockIdx.x;
-    if (pos0 < T) {
-      bool nb;
-      uint32_t ng, ns;
-      decode32(pos0, nb, ng, ns);
-      pre_ctr = ctr_of(nb, ng);
-      if (pre_ctr != nullptr) pre_val = ld_acquire(pre_ctr);
-    }
-    for (int i = 0; i < NBUF - 1; ++i) claim(i);
-  }
-  __syncthreads();
-  bool nonfinite = false;
-  int phase_bits = 0;
-  for (uint32_t k = 0;; ++k) {
-    const int b = (int)(k % NBUF);
-    if (threadIdx.x == 0) {
-      claim((int)((k + NBUF - 1) % NBUF));  // refill the buffer freed by task k-1
-      if (t_grp[b] >= 0 && !t_issued[b]) {  // task k's producers were late: wait now
-        const int32_t* ctr = ctr_of(t_isB[b], (uint32_t)t_grp[b]);
-        const int32_t need = t_isB[b] ? (int32_t)TAn : (int32_t)TBn;
-        while (ld_acquire(ctr) < need) __nanosleep(64);
-        fence_proxy_async();
-        issue(b);
-      }
-    }
-    __syncthreads();
-    const int grp = t_grp[b];
-    if (grp < 0) break;
-    const bool isB = t_isB[b];
-    const int sub = t_sub[b], slot = t_slot[b];
-    mbar_wait(&full[b], (uint32_t)((phase_bits >> b) & 1));
-    phase_bits ^= 1 << b;
-    V* buf = bufs + b * BUF;
-    if (!isB) {
-      TA::run_smem(p.a, p, grp, sub, slot, buf, twA, nonfinite, nullptr, nullptr);
-      __syncthreads();
-      if (threadIdx.x == 0) red_release_add(p.doneA + grp, 1);
-    } else {
-      const V* stg = (const V*)p.staging + (int64_t)slot * p.slot_elems + (int64_t)sub * p.b.it;
-      TB::run_smem(p.b, p, grp, sub, slot, buf, twB, nonfinite, p.doneB + grp, stg);
-      __syncthreads();
-    }
-  }
-  if (__syncthreads_or(nonfinite) && threadIdx.x == 0) atomicOr(p.flag, 1);
-}
-
-// TMA-prefetching DIRECT pass (one tile type, no staging, no dependencies):
-// static round-robin schedule (task = blockIdx + k*gridDim), thread 0 keeps
-// NBUF-1 tiles in flight with one TMA tensor copy each, all threads compute.
-template <typename R, class TA, int NBUF>
-__global__ void __launch_bounds__(TA::NT, 1) tpd_kernel(const __grid_constant__ PassArgs p) {
-  using V = typename CT<R>::V;
-  static_assert(TA::SWZ && TA::TOFF == 0, "TMA tiles, all threads compute");
-  extern __shared__ __align__(128) unsigned char smem_raw[];
-  constexpr int BUF = TA::SMEM_ELEMS;
-  static_assert((BUF * sizeof(V)) % 1024 == 0, "swizzled buffers stay 1024-byte aligned");
-  V* bufs = reinterpret_cast<V*>(smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u));
-  V* tw = bufs + NBUF * BUF;
-  __shared__ __align__(8) uint64_t full[NBUF];
-  if (threadIdx.x == 0)
-    for (int i = 0; i < NBUF; ++i) mbar_init(&full[i], 1);
-  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  TA::build_table(tw);
-  const uint64_t pol = policy_evict_first();
-  const int64_t T = p.total_tasks;
-  auto issue = [&](int64_t task, int b) {
-    if (task >= T) return;
-    V* dst = bufs + b * BUF;
-    constexpr int BOX = TA::RHO > 256 ? TA::RHO / 2 : TA::RHO;
-    mbar_arrive_tx(&full[b], (uint32_t)(TA::D * TA::RHO * 128));
-#pragma unroll
-    for (int h = 0; h < TA::RHO / BOX; ++h)
-      tma_load_3d(dst + h * BOX * TA::D * TA::F, &p.tmA, 0, (int)(task * TA::D), h * BOX, &full[b], pol);
-  };
-  if (threadIdx.x == 0)
-    for (int i = 0; i < NBUF - 1; ++i) issue(blockIdx.x + (int64_t)i * gridDim.x, i);
-  __syncthreads();
-  bool nonfinite = false;
-  int phase_bits = 0;
-  for (int64_t k = 0;; ++k) {
-    const int64_t task = blockIdx.x + k * gridDim.x;
-    if (task >= T) break;
-    const int b = (int)(k % NBUF);
-    if (threadIdx.x == 0) issue(blockIdx.x + (k + NBUF - 1) * gridDim.x, (int)((k + NBUF - 1) % NBUF));
-    mbar_wait(&full[b], (uint32_t)((phase_bits >> b) & 1));
-    phase_bits ^= 1 << b;
-    TA::run_smem(p.a, p, task, 0, 0, bufs + b * BUF, tw, nonfinite, nullptr, nullptr);
-    __syncthreads();
-  }
-  if (__syncthreads_or(nonfinite) && threadIdx.x == 0) atomicOr(p.flag, 1);
-}
-
 // ----------------------------------------------------------------------------
 // Block permutations used by the sharded (multi-GPU) six-step: pack/unpack of
 // all-to-all chunks.  Elements are opaque 8- or 16-byte words (VT).

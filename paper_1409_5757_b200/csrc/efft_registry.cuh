@@ -25,31 +25,16 @@ template <typename R, int RHO, bool MASK> using T3 = Tile<R, RHO, 384 / RHO, 256
 // lane access.
 template <typename R, int RHO> using ST = Tile<R, RHO, (RHO % 3 ? 512 : 384) / RHO, 256, false, 1, 32, 1, true>;
 
-template <typename R, class TA, class TB, bool WS = false, bool PF = false, int NBUF = 2, bool TP = false,
-          bool TPD = false>
+template <typename R, class TA, class TB, bool WS = false, int NBUF = 2>
 KernelInfo make_info() {
   using V = typename CT<R>::V;
   KernelInfo k{};
   const int sm = TA::SMEM_ELEMS > TB::SMEM_ELEMS ? TA::SMEM_ELEMS : TB::SMEM_ELEMS;
-  if constexpr (TPD) {
-    k.fn = tpd_kernel<R, TA, NBUF>;
-    k.nt = TA::NT;
-    k.smem_bytes = (int)((NBUF * TA::SMEM_ELEMS + TA::RHO) * sizeof(V)) + 1024;
-    k.ws = 2;  // direct TMA tensor map
-  } else if constexpr (TP) {
-    k.fn = tp_kernel<R, TA, TB, NBUF>;
-    k.nt = TA::NT;
-    k.smem_bytes = (int)((NBUF * sm + TA::RHO + TB::RHO) * sizeof(V)) + 1024;
-    k.ws = 1;  // uses the TMA tensor maps
-  } else if constexpr (WS) {
+  if constexpr (WS) {
     k.fn = staged_kernel<R, TA, TB, NBUF>;
     k.nt = TA::NT + 32;
     k.smem_bytes = (int)((NBUF * sm + TA::RHO + TB::RHO) * sizeof(V)) + 1024;  // + swizzle alignment slack
     k.ws = 1;
-  } else if constexpr (PF) {
-    k.fn = pf_kernel<R, TA, TB>;
-    k.nt = TA::NT;
-    k.smem_bytes = (int)((sm + TA::RHO + TB::RHO) * sizeof(V));
   } else {
     k.fn = pass_kernel<R, TA, TB>;
     k.nt = TA::NT;
@@ -74,15 +59,7 @@ KernelInfo make_info() {
 // Defined in inst_f32.cu / inst_f64.cu.
 bool get_direct_kernel_f32(int rho, KernelInfo* out);
 bool get_direct_kernel_f64(int rho, KernelInfo* out);
-bool get_staged_kernel_f32(int rho_a, int rho_b, int ws, KernelInfo* out);
-bool get_staged_kernel_f64(int rho_a, int rho_b, int ws, KernelInfo* out);
-bool get_staged_small_f32(int rho_b, KernelInfo* out);
-bool get_staged_wide_f32(int rho_b, KernelInfo* out);
-bool get_staged_pf_f32(int rho_b, KernelInfo* out);
-bool get_staged_pf_f64(int rho_b, KernelInfo* out);
-bool get_staged_tp_f32(int rho_b, KernelInfo* out);
-bool get_staged_ws32_f32(int rho_b, KernelInfo* out);
-bool get_direct_tp_f32(int rho, KernelInfo* out);
-bool get_staged_tp_f64(int rho_b, KernelInfo* out);
+bool get_staged_kernel_f32(int rho_a, int rho_b, KernelInfo* out);
+bool get_staged_kernel_f64(int rho_a, int rho_b, KernelInfo* out);
 
 }  // namespace efft
