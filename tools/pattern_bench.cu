@@ -62,21 +62,21 @@ __device__ __forceinline__ void st4(float4* p, float4 v) {
 }
 // 16-byte lanes: 8 lanes per 128-byte line; a unit = 512 lines (256 threads x 16 loads / 8)
 __global__ void __launch_bounds__(256) pat16(const float2* __restrict__ src, float2* __restrict__ dst, int64_t n,
-                                             int64_t C, int mode, int64_t nunits) {
-  const int lane = threadIdx.x & 7, grp = threadIdx.x >> 3;  // 32 line-groups per CTA
+                                             int64_t C, int mode, int64_t nunits, int W = 1) {
+  const int lane = threadIdx.x % (8 * W), grp = threadIdx.x / (8 * W);  // 32/W segment-groups per CTA
   const int64_t R = n / C;
   for (int64_t u = blockIdx.x; u < nunits; u += gridDim.x) {
     float4 v[16];
 #pragma unroll
     for (int t = 0; t < 16; ++t) {
-      const int64_t i = u * 512 + grp + 32 * t;
-      const int64_t off = mode == 1 ? (i / R) * 16 + (i % R) * C : i * 16;
+      const int64_t i = u * (512 / W) + grp + (32 / W) * t;  // segment id
+      const int64_t off = mode == 1 ? (i / R) * 16 * W + (i % R) * C : i * 16 * W;
       v[t] = ld4(reinterpret_cast<const float4*>(src + off) + lane);
     }
 #pragma unroll
     for (int t = 0; t < 16; ++t) {
-      const int64_t i = u * 512 + grp + 32 * t;
-      st4(reinterpret_cast<float4*>(dst + i * 16) + lane, v[t]);
+      const int64_t i = u * (512 / W) + grp + (32 / W) * t;
+      st4(reinterpret_cast<float4*>(dst + i * 16 * W) + lane, v[t]);
     }
   }
 }
@@ -94,7 +94,7 @@ int main() {
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
-  for (int mode : {0, 1, 6, 7})
+  for (int mode : {0, 1})
     for (int64_t C : {1ll << 15, 1ll << 12, 1ll << 8})
       for (int occ : {4, 8}) {
         if (C != (1ll << 15)) continue;
@@ -110,19 +110,20 @@ int main() {
         printf("mode=%d C=2^%d ctas/sm=%d: %.3f ms  %.0f GB/s\n", mode, __builtin_ctzll(C), occ, ms,
                2.0 * n * 8 / (ms * 1e-3) / 1e9);
       }
+  for (int W : {1, 2, 4})
   for (int mode : {0, 1})
-    for (int occ : {2, 4}) {
+    for (int occ : {4}) {
       const int grid = sms * occ;
       const int64_t nu = n / 16 / 512;
-      pat16<<<grid, 256>>>(a, b, n, 1ll << 15, mode, nu);
+      pat16<<<grid, 256>>>(a, b, n, 1ll << 15, mode, nu, W);
       cudaEventRecord(e0);
-      for (int r = 0; r < 3; ++r) pat16<<<grid, 256>>>(a, b, n, 1ll << 15, mode, nu);
+      for (int r = 0; r < 3; ++r) pat16<<<grid, 256>>>(a, b, n, 1ll << 15, mode, nu, W);
       cudaEventRecord(e1);
       cudaEventSynchronize(e1);
       float ms;
       cudaEventElapsedTime(&ms, e0, e1);
       ms /= 3;
-      printf("16B lanes mode=%d ctas/sm=%d: %.3f ms  %.0f GB/s\n", mode, occ, ms, 2.0 * n * 8 / (ms * 1e-3) / 1e9);
+      printf("16B lanes segment=%dB mode=%d ctas/sm=%d: %.3f ms  %.0f GB/s\n", 128 * W, mode, occ, ms, 2.0 * n * 8 / (ms * 1e-3) / 1e9);
     }
   // L2-resident copies (32 MB and 16 MB buffers, repeated): L2 read+write bandwidth
   for (int64_t m : {1ll << 22, 1ll << 21, 1ll << 20})
