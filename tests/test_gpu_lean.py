@@ -1,10 +1,11 @@
 """The lean staged passes (paper_1409_5757_b200/csrc/lean.cu) vs the oracle -- needs a B200.
 
-The planner routes power-of-two complex64 / complex128 transforms with
-2^26 <= N <= 2^32 to the lean kernels; these tests pin them at sizes the fp64
-oracle (oracle/efft_oracle.c) finishes in seconds, for both directions, both
-pass shapes (R1 = R2 and R1 = 2 R2), the non-finite input flag and the
-agreement with the generic staged kernels (EFFT_LEAN=0).
+The planner routes complex64 / complex128 transforms with 2^26 <= N <= 2^32
+and 3*2^24 <= N <= 3*2^30 to the lean kernels; these tests pin them at sizes
+the fp64 oracle (oracle/efft_oracle.c) finishes in seconds, for both
+directions, both pass shapes (R1 = R2 and R1 = 2 R2), the radix-3 family, the
+non-finite input flag and the agreement with the generic staged kernels
+(EFFT_LEAN=0).
 Tolerances as in test_gpu_parity.py: rel-L2 <= 1e-12 log2N (c128), 1e-5 log2N (c64).
 """
 import math
@@ -57,6 +58,19 @@ def test_lean_forward_inverse_vs_oracle(lg, dtype):
 
 
 @pytest.mark.parametrize("dtype", ["complex64", "complex128"])
+@pytest.mark.parametrize("n", [3 << 24, 3 << 25])
+def test_lean_radix3_family_vs_oracle(n, dtype):
+    """N = 3 * 2^k: pass 1 runs rho_a = 192 = 16 x 12 tiles."""
+    x = random_c(n, seed=n % 1000)
+    xd = torch.from_numpy(x.astype(NP[dtype])).cuda()
+    p, y = run(xd, dtype)
+    assert "rho_a=192" in p.describe()
+    assert oracle.rel_l2(y.cpu().numpy(), oracle.transform(x)) <= tol(n, dtype)
+    _, z = run(y, dtype, direction=1)
+    assert oracle.rel_l2(z.cpu().numpy(), x) <= 2 * tol(n, dtype)
+
+
+@pytest.mark.parametrize("dtype", ["complex64", "complex128"])
 def test_lean_agrees_with_generic_staged_path(dtype, monkeypatch):
     n = 1 << 26
     x = torch.from_numpy(random_c(n, seed=7).astype(NP[dtype])).cuda()
@@ -88,15 +102,16 @@ def test_lean_structured_inputs_exact_bins():
     assert mag.max().item() / n < 1e-11
 
 
-def test_lean_nonfinite_flag():
-    n = 1 << 26
-    x = torch.zeros(n, dtype=torch.complex64, device="cuda")
-    x[12345] = float("nan")
-    p, _ = run(x, "complex64", flags=1)  # EFFT_FLAG_CHECK_FINITE
+@pytest.mark.parametrize("n,dtype", [(1 << 26, "complex64"), (1 << 26, "complex128"), (3 << 24, "complex128")])
+def test_lean_nonfinite_flag(n, dtype):
+    x = torch.zeros(n, dtype=TT[dtype], device="cuda")
+    x[12345] = float("inf")
+    p, _ = run(x, dtype, flags=1)  # EFFT_FLAG_CHECK_FINITE
     assert p.nonfinite_seen(torch.cuda.current_stream().cuda_stream)
     x[12345] = 0
     p.execute(x.data_ptr(), torch.empty_like(x).data_ptr(), torch.cuda.current_stream().cuda_stream)
     assert not p.nonfinite_seen(torch.cuda.current_stream().cuda_stream)
+    assert "lean" in p.describe()
 
 
 @pytest.mark.slow
