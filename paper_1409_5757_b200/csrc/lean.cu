@@ -260,14 +260,20 @@ __global__ void __launch_bounds__(LT<R>::NT, MINB) lean_pass(const __grid_consta
   using V = typename LT<R>::V;
   constexpr int F = LT<R>::F, NT = LT<R>::NT, PITCH = LT<R>::PITCH;
   constexpr int S = RA / 16, QB = RB / 16, DB = 16 / QB;
+  // A tile: jb = s + A1 t (s < A1 rows of threads, t < A0), stage 0 = A0-point
+  // DFT over t, stage 1 = A1-point DFT over s, kb = kt + A0 ks.  RA = 192 runs
+  // 12 x 16 in the in-place pass (every thread row loads) and 16 x 12 in the
+  // transposing one (its output lines need 16 consecutive kt).
+  constexpr int A0 = (RA == 256 || T1) ? 16 : RA / 16, A1 = RA / A0;
   extern __shared__ __align__(128) unsigned char smraw[];
   V* xb = reinterpret_cast<V*>(smraw);
-  V* w256 = xb + LT<R>::XB;  // W_256^i      (B inner twiddle, W_RB = W_256^(256/RB))
+  constexpr int XBN = T1 ? LT<R>::XB : 256 * LT<R>::F;  // the plain exchange needs no padding
+  V* w256 = xb + XBN;        // W_256^i      (B inner twiddle, W_RB = W_256^(256/RB))
   V* wlo = w256 + 256;       // W_R^i, i < 256
   // W_(R/256)^i, i < R/256 and W_RA^i, i < RA (A inner twiddle): own tables
   // only when RA = 192; for RA = 256 both are strided views of W_256
   V* whi = RA == 256 ? w256 : wlo + 256;
-  V* wa = RA == 256 ? w256 : wlo + 512;
+  V* wa = RA == 256 ? w256 : wlo + 256 + 192;
   constexpr int HS = RA == 256 ? 256 / RB : 1;  // stride of whi
   __shared__ SchedShared shs;
   const int tid = threadIdx.x, lane = tid % F, r = tid / F;
@@ -280,8 +286,10 @@ __global__ void __launch_bounds__(LT<R>::NT, MINB) lean_pass(const __grid_consta
     w256[i] = to_v(wroot(i, 256), R());
     wlo[i] = to_v(wroot(i, a.R), R());
     if constexpr (RA != 256) {
-      whi[i] = to_v(wroot(i, a.R / 256), R());
-      wa[i] = to_v(wroot(i, RA), R());
+      if (i < 192) {  // R / 256 = 192 RB / 256 <= 192 and RA = 192 entries
+        whi[i] = to_v(wroot(i, a.R / 256), R());
+        wa[i] = to_v(wroot(i, RA), R());
+      }
     }
   }
   Sched sc{&shs};
@@ -296,12 +304,12 @@ __global__ void __launch_bounds__(LT<R>::NT, MINB) lean_pass(const __grid_consta
       for (int dl = 0; dl < DB; ++dl)
 #pragma unroll
         for (int q = 0; q < QB; ++q) v[dl * QB + q] = ld_staging(sp + b_line<R, RA, RB, T1>(task, dl, r, q, lane));
-    } else if (r < S) {  // A: jb = s + S t with s = r
+    } else if (r < A1) {  // A: jb = s + A1 t with s = r
       const uint64_t pol = policy_evict_first();
       const V* p0 = SRC + (int64_t)g * F + lane + a.LS * (int64_t)(task + RB * r);
-      const int64_t step = a.LS * (int64_t)(RB * S);
+      const int64_t step = a.LS * (int64_t)(RB * A1);
 #pragma unroll
-      for (int t = 0; t < 16; ++t) v[t] = ld_hbm(p0 + t * step, pol);
+      for (int t = 0; t < A0; ++t) v[t] = ld_hbm(p0 + t * step, pol);
     }
     sc.after_loads(a, isB, g);
     if (isB) {
@@ -345,31 +353,31 @@ __global__ void __launch_bounds__(LT<R>::NT, MINB) lean_pass(const __grid_consta
       for (int dl = 0; dl < DB; ++dl)
 #pragma unroll
         for (int k = 0; k < QB; ++k) xb[((dl * QB + k) * 16 + r) * F + lane] = v[dl * QB + P<QB>(k)];
-    } else if (r < S) {
-      // ---- sub-stage A, stage 0: 16-point DFT over t, W_RA^(s kt)
+    } else if (r < A1) {
+      // ---- sub-stage A, stage 0: A0-point DFT over t, W_RA^(s kt)
       if (a.check_finite) {
 #pragma unroll
-        for (int t = 0; t < 16; ++t) nf |= !(isfinite(v[t].x) && isfinite(v[t].y));
+        for (int t = 0; t < A0; ++t) nf |= !(isfinite(v[t].x) && isfinite(v[t].y));
       }
       if constexpr (T1) {
 #pragma unroll
-        for (int t = 0; t < 16; ++t) v[t] = cscale(v[t], cvt(a.cin, R()));
+        for (int t = 0; t < A0; ++t) v[t] = cscale(v[t], cvt(a.cin, R()));
       }
-      reg_dft<R, 16>(v);
+      reg_dft<R, A0>(v);
       {
         const V* wp = wa;
 #pragma unroll
-        for (int k = 1; k < 16; ++k) {
+        for (int k = 1; k < A0; ++k) {
           wp += r;
-          v[P<16>(k)] = cmul(v[P<16>(k)], *wp);
+          v[P<A0>(k)] = cmul(v[P<A0>(k)], *wp);
         }
       }
 #pragma unroll
-      for (int k = 0; k < 16; ++k) {
+      for (int k = 0; k < A0; ++k) {
         if constexpr (T1)
-          xb[(r * 16 + k) * PITCH + lane] = v[P<16>(k)];  // [s][kt][j2l]
+          xb[(r * 16 + k) * PITCH + lane] = v[P<A0>(k)];  // [s][kt][j2l]
         else
-          xb[(k * S + r) * F + lane] = v[P<16>(k)];  // [kt][s][lane]
+          xb[(k * A1 + r) * F + lane] = v[P<A0>(k)];  // [kt][s][lane]
       }
     }
     sc.before_exchange(a, g);
@@ -402,19 +410,19 @@ __global__ void __launch_bounds__(LT<R>::NT, MINB) lean_pass(const __grid_consta
 #pragma unroll
         for (int kp = 0; kp < 16; ++kp) st_hint(op + kp * step, cscale(v[P<16>(kp)], cvt(a.cout, R())), pol);
       }
-    } else {
-      // ---- sub-stage A, stage 1: S-point DFT over s -> ks, store to the ring
-      // T0 thread (lane, kt = r): ring [kb][ja][lane], kb = kt + 16 ks
+    } else if (T1 || r < A0) {
+      // ---- sub-stage A, stage 1: A1-point DFT over s -> ks, store to the ring
+      // T0 thread (lane, kt = r): ring [kb][ja][lane], kb = kt + A0 ks
       // T1 thread (kt = tid % 16, j2l = tid / 16): ring [j2l][ja][ks][kt]
       const int kt = T1 ? tid % 16 : r, j2l = tid / 16;
 #pragma unroll
-      for (int u = 0; u < S; ++u) v[u] = T1 ? xb[(u * 16 + kt) * PITCH + j2l] : xb[(kt * S + u) * F + lane];
-      reg_dft<R, S>(v);
-      const int base = T1 ? (j2l * RB + task) * (16 * S) + kt : (kt * RB + task) * F + lane;
-      const int step = T1 ? 16 : 16 * RB * F;
+      for (int u = 0; u < A1; ++u) v[u] = T1 ? xb[(u * 16 + kt) * PITCH + j2l] : xb[(kt * A1 + u) * F + lane];
+      reg_dft<R, A1>(v);
+      const int base = T1 ? (j2l * RB + task) * (16 * A1) + kt : (kt * RB + task) * F + lane;
+      const int step = T1 ? 16 : A0 * RB * F;
       const uint64_t keep = policy_evict_last();
 #pragma unroll
-      for (int ks = 0; ks < S; ++ks) st_hint(sp + base + ks * step, v[P<S>(ks)], keep);
+      for (int ks = 0; ks < A1; ++ks) st_hint(sp + base + ks * step, v[P<A1>(ks)], keep);
     }
     sc.end(a, isB, g);
   }
@@ -701,12 +709,23 @@ void build_tables(void* t4, int64_t n, int c128, cudaStream_t s) {
 
 template <typename R, int RA>
 static void* pick_ra(int rb, bool t1) {
-  switch (rb) {
-    case 32: return t1 ? (void*)lean_pass<R, RA, 32, true, 4> : (void*)lean_pass<R, RA, 32, false, 4>;
-    case 64: return t1 ? (void*)lean_pass<R, RA, 64, true, 4> : (void*)lean_pass<R, RA, 64, false, 4>;
-    case 128: return t1 ? (void*)lean_pass<R, RA, 128, true, 4> : (void*)lean_pass<R, RA, 128, false, 4>;
-    case 256: return t1 ? (void*)lean_pass<R, RA, 256, true, 4> : (void*)lean_pass<R, RA, 256, false, 4>;
-    default: return nullptr;
+  if constexpr (RA == 192) {  // the factor 3 runs in the in-place pass only
+    if (t1) return nullptr;
+    switch (rb) {
+      case 32: return (void*)lean_pass<R, 192, 32, false, 4>;
+      case 64: return (void*)lean_pass<R, 192, 64, false, 4>;
+      case 128: return (void*)lean_pass<R, 192, 128, false, 4>;
+      case 256: return (void*)lean_pass<R, 192, 256, false, 4>;
+      default: return nullptr;
+    }
+  } else {
+    switch (rb) {
+      case 32: return t1 ? (void*)lean_pass<R, RA, 32, true, 4> : (void*)lean_pass<R, RA, 32, false, 4>;
+      case 64: return t1 ? (void*)lean_pass<R, RA, 64, true, 4> : (void*)lean_pass<R, RA, 64, false, 4>;
+      case 128: return t1 ? (void*)lean_pass<R, RA, 128, true, 4> : (void*)lean_pass<R, RA, 128, false, 4>;
+      case 256: return t1 ? (void*)lean_pass<R, RA, 256, true, 4> : (void*)lean_pass<R, RA, 256, false, 4>;
+      default: return nullptr;
+    }
   }
 }
 // 4 CTAs per SM for both types (complex64: 64 registers per thread; complex128
@@ -740,12 +759,13 @@ bool plan(int64_t n, int c128, int inverse, bool scale_inverse, bool check_finit
     ++t;
   }
   if (m != 1 && m != 3) return false;
-  // pass 1: RA1 = 256 (192 when 3 | n), pass 2: RA2 = 256; log2(RB1 RB2) = t - 16 (or t - 14)
-  const int ra1 = m == 3 ? 192 : 256;
+  // RA = 256, except RA = 192 in pass 2 (the in-place pass) when 3 | n;
+  // log2(RB1 RB2) = t - 16 (or t - 14)
+  const int ra2 = m == 3 ? 192 : 256;
   const int lbs = m == 3 ? t - 14 : t - 16;
   const int lb1 = (lbs + 1) / 2, lb2 = lbs - lb1;
   if (lb1 < 5 || lb1 > 8 || lb2 < 5 || lb2 > 8) return false;
-  const int64_t R1 = (int64_t)ra1 << lb1, R2 = int64_t(256) << lb2;
+  const int64_t R1 = int64_t(256) << lb1, R2 = (int64_t)ra2 << lb2;
   const int F = c128 ? 8 : 16, NT = 16 * F;
   const size_t elem = c128 ? 16 : 8;
   int64_t stg = 0;
@@ -753,14 +773,16 @@ bool plan(int64_t n, int c128, int inverse, bool scale_inverse, bool check_finit
     Pass& q = p[i];
     const bool t1 = i == 0;
     const int64_t R = t1 ? R1 : R2;
-    q.ra = t1 ? ra1 : 256;
+    q.ra = t1 ? 256 : ra2;
     q.rb = 1 << (t1 ? lb1 : lb2);
     const bool paired = !c128 && q.ra == 256 && use_pair();
     q.fn = reinterpret_cast<void (*)(Args)>(paired ? pick_pair(q.rb, t1)
                                             : c128 ? pick<double>(q.ra, q.rb, t1) : pick<float>(q.ra, q.rb, t1));
     if (!q.fn) return false;
     q.nt = paired ? pair::NT : NT;
-    q.smem = paired ? (int)((pair::XB2 + 512) * elem) : (int)((256 * (F + 1) + (q.ra == 256 ? 2 : 4) * 256) * elem);
+    // exchange (padded only in the transposing pass) + W_256 + W_R^(i<256) (+ two 192-entry tables)
+    q.smem = paired ? (int)((pair::XB2 + 512) * elem)
+                    : (int)(((t1 ? 256 * (F + 1) : 256 * F) + 512 + (q.ra == 256 ? 0 : 2 * 192)) * elem);
     Args& a = q.a;
     a = Args{};
     a.R = R;
