@@ -481,7 +481,7 @@ __global__ void __launch_bounds__(pair::NT, 4) lean_pair(const __grid_constant__
   extern __shared__ __align__(128) unsigned char smraw[];
   V* xb = reinterpret_cast<V*>(smraw);
   float4* xq = reinterpret_cast<float4*>(smraw);
-  V* w256 = xb + pair::XB2;
+  V* w256 = xb + (T1 ? pair::XB2 : 4096);  // the plain exchange needs no padding
   V* wlo = w256 + 256;
   __shared__ SchedShared shs;
   const int tid = threadIdx.x, cp = tid % 8, r = tid / 8;
@@ -781,7 +781,7 @@ bool plan(int64_t n, int c128, int inverse, bool scale_inverse, bool check_finit
     if (!q.fn) return false;
     q.nt = paired ? pair::NT : NT;
     // exchange (padded only in the transposing pass) + W_256 + W_R^(i<256) (+ two 192-entry tables)
-    q.smem = paired ? (int)((pair::XB2 + 512) * elem)
+    q.smem = paired ? (int)(((t1 ? pair::XB2 : 4096) + 512) * elem)
                     : (int)(((t1 ? 256 * (F + 1) : 256 * F) + 512 + (q.ra == 256 ? 0 : 2 * 192)) * elem);
     Args& a = q.a;
     a = Args{};
