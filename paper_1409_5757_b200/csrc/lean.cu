@@ -1,43 +1,47 @@
-// lean.cu -- lean staged passes for the large power-of-two DFTs (complex64 and
-// complex128, 2^26 <= N <= 2^32).
+// lean.cu -- lean staged passes for the large DFTs: complex64 and complex128,
+// N = 2^k (2^26 <= N <= 2^32) and N = 3 * 2^k (3 * 2^24 <= N <= 3 * 2^30).
 //
 // Same algorithm as the generic staged pass (efft_kernels.cuh: the four-step
 // form of the reference's scatter -> leaves -> merges, scatter.py:31-57,
 // leaf_dft.py:93-125, recombine.py:144-260), specialised so that a tile costs
-// as few issue slots and registers as possible:
-//   * 16 complex elements per thread; a tile is F lanes (F = one 128-byte line:
-//     16 c64 / 8 c128) x 256 points, 16F threads, 4 CTAs per SM;
-//   * every global access is one element per lane, F lanes covering one
-//     128-byte line, so the 16 points a thread owns for its first radix stage
-//     come straight from HBM / L2 into registers;
-//   * exactly one shared-memory exchange per sub-stage (one STS + one LDS per
-//     element); the transposing exchange uses a row pitch of F+1 so both sides
-//     are bank-conflict free;
-//   * radix-16 / radix-QB register DFTs (paired-fp32 FADD2/FFMA2 for c64);
+// as few issue slots, registers and memory requests as possible:
+//   * a tile is F columns (F = one 128-byte line: 16 c64 / 8 c128) x 256
+//     points (32 KB), 4 CTAs per SM;
+//   * lean_pass (complex128, and the 3 * 2^k pass): one element per lane, 16
+//     points per thread, 16F threads;  lean_pair (complex64): two adjacent
+//     columns per thread, 32 points per thread, 128 threads, so every HBM / L2
+//     access is 16 bytes (8 lanes per line);
+//   * the points a thread owns for its first radix stage come straight from
+//     HBM / L2 into registers; exactly one shared-memory exchange per
+//     sub-stage; the transposing exchange uses padded rows so both sides are
+//     bank-conflict free;
+//   * radix-16 / 12 / QB register DFTs (paired-fp32 FADD2/FFMA2 for c64);
 //   * twiddles from fp64-built tables (W_256 and W_R^(i<256) in shared memory,
 //     three 2048-entry levels of W_N in a 48/96 KB plan buffer) with short
 //     recurrences: no N-sized twiddle array is read.
 //
-// Index maps (N = R1 R2, R = 256 RB per pass, j = ja + RB jb, k = kb + 256 ka,
-// jb = s + 16 t, kb = kt + 16 ks, ja = p + 16 q, ka = kq + QB kp, QB = RB/16):
+// Index maps (N = R1 R2, R = RA RB per pass, j = ja + RB jb, k = kb + RA ka,
+// jb = s + A1 t, kb = kt + A0 ks (RA = A0 A1: 16 x 16, or 12 x 16 for the
+// factor 3), ja = p + 16 q, ka = kq + QB kp, QB = RB/16):
 //   pass 1 (T1):  x[j2 + R2 j1] -> y[k1 + R1 j2] * W_N^(j2 k1); group = F j2
 //   pass 2 (T0):  y[k1 + R1 j2] -> X[k1 + R1 k2] in place;      group = F k1
-// Sub-stage A (per group: RB tiles of F lanes x 256 jb, one ja each):
-//   16-point DFT over t, W_256^(s kt), exchange, 16-point DFT over s, store to
+// Sub-stage A (per group: RB tiles of F lanes x RA jb, one ja each):
+//   A0-point DFT over t, W_RA^(s kt), exchange, A1-point DFT over s, store to
 //   the group's L2 staging slot (T1: lanes become kt -- the j2 <-> k1 transpose).
-// Sub-stage B (per group: RB tiles of F lanes x RB ja x DB = 16/QB kb or j2):
+// Sub-stage B (per group: RA RB / 256 tiles of F lanes x RB ja x DB = 16/QB kb or j2):
 //   W_R^(ja kb), QB-point DFTs over q, W_RB^(p kq), exchange, 16-point DFT over
 //   p, (T1: W_N^(j2 k1)), store to HBM.
 //
 // Scheduling: one persistent kernel per pass.  Tasks are claimed from a
-// counter in the order A(0..lag-1), [B(g-lag) x RB, A(g) x RB] pairs, the tail
-// of B; B(g) needs A(g) complete, A(g)'s staging stores need the slot released
-// by B(g - nslots).  Every dependency points to an earlier position and a
-// CTA's claims increase, so the smallest unfinished task can always run
+// counter in the order A(0..lag-1), [B(g-lag), A(g)] blocks, the tail of B;
+// B(g) needs A(g) complete, A(g)'s staging stores need the slot released by
+// B(g - nslots).  Every dependency points to an earlier position and a CTA's
+// claims increase, so the smallest unfinished task can always run
 // (deadlock-free; a CTA never blocks while holding an unreleased finished
-// tile).  Thread 0 keeps synchronisation off the critical path: claims run two
-// tasks ahead, the next task's producers are probed with an acquire load issued
-// beside the tile loads, and tile k is released in the middle of tile k+1.
+// tile).  Thread 0 keeps synchronisation off the critical path (Sched below):
+// claims run two tasks ahead, the next task's producers are probed with
+// relaxed loads, and ONE fence.acq_rel per tile, issued right after the tile
+// loads, releases the previous tile and completes those acquires.
 #include <cstdlib>
 
 #include "efft_kernels.cuh"
@@ -168,8 +172,8 @@ __device__ __forceinline__ int b_line(int task, int dl, int p, int q, int lane) 
 
 // Per-CTA task scheduling shared by the tile kernels (see the header comment):
 // dynamic claims two ahead, decoded once by thread 0 into shared memory;
-// acquire probes issued beside the tile loads; release of tile k deferred to
-// the middle of tile k+1.
+// relaxed probes of the next task's producers at the loop top; one fence per
+// tile right after the tile loads (release of tile k-1, acquire of the probes).
 struct SchedShared {
   int ready, isB[2], g[2], task[2];
   long long pos[2];
@@ -203,7 +207,7 @@ struct Sched {
   // loop top (all threads): the current task, or false when the pass is done.
   // Thread 0 also claims the task after next and probes (relaxed) the next
   // task's producers and this A task's staging slot; the fence in
-  // before_exchange() completes those acquires before anything depends on them.
+  // after_loads() completes those acquires before anything depends on them.
   __device__ __forceinline__ bool next(const Args& a, int& isB, int& g, int& task) {
     if (sh->pos[cb] >= a.total) return false;
     isB = sh->isB[cb];
