@@ -87,6 +87,15 @@ int efft_execute(efft_plan_t plan, const void *d_in, void *d_out, void *stream);
  * and an inverse plan of the same size need one pair between them. */
 int efft_execute_host(efft_plan_t plan, const void *h_in, void *h_out, void *stream);
 
+/* `count` end-to-end transforms with host buffers (h_in[k] -> h_out[k]),
+ * pipelined: transform k+1's host-to-device copy runs on an internal copy
+ * stream while transform k computes and copies back on `stream`, so both PCIe
+ * directions are busy at once (two device in/out pairs, allocated per call;
+ * falls back to one-at-a-time efft_execute_host when they do not fit).
+ * Returns after the last copy-back has completed. */
+int efft_execute_host_batch(efft_plan_t plan, const void *const *h_in, void *const *h_out, int count,
+                            void *stream);
+
 /* Frees the per-device pool of efft_execute_host (it is re-created on demand). */
 int efft_release_host_buffers(int device);
 

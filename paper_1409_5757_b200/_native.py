@@ -43,6 +43,7 @@ EXPORTED = (
     "efft_execute",
     "efft_execute_host",
     "efft_release_host_buffers",
+    "efft_execute_host_batch",
     "efft_nonfinite_seen",
     "efft_plan_destroy",
     "efft_plan_enable_timing",
@@ -78,6 +79,7 @@ def load():
     lib.efft_execute.argtypes = [vp, vp, vp, vp]
     lib.efft_execute_host.argtypes = [vp, vp, vp, vp]
     lib.efft_release_host_buffers.argtypes = [i32]
+    lib.efft_execute_host_batch.argtypes = [vp, ctypes.POINTER(vp), ctypes.POINTER(vp), i32, vp]
     lib.efft_nonfinite_seen.argtypes = [vp, ctypes.POINTER(i32), vp]
     lib.efft_plan_destroy.argtypes = [vp]
     lib.efft_plan_enable_timing.argtypes = [vp, i32]
@@ -157,6 +159,13 @@ class NativePlan:
 
     def execute_host(self, h_in: int, h_out: int, stream: int) -> None:
         check(load().efft_execute_host(self._h, h_in, h_out, stream), "efft_execute_host")
+
+    def execute_host_batch(self, h_in: list, h_out: list, stream: int) -> None:
+        """Pipelined end-to-end transforms h_in[k] -> h_out[k] (host pointers)."""
+        k = len(h_in)
+        arr_in = (ctypes.c_void_p * k)(*h_in)
+        arr_out = (ctypes.c_void_p * k)(*h_out)
+        check(load().efft_execute_host_batch(self._h, arr_in, arr_out, k, stream), "efft_execute_host_batch")
 
     def nonfinite_seen(self, stream: int) -> bool:
         v = ctypes.c_int()

@@ -815,6 +815,72 @@ int efft_execute_host(efft_plan_t pl, const void* h_in, void* h_out, void* strea
   return EFFT_OK;
 }
 
+int efft_execute_host_batch(efft_plan_t pl, const void* const* h_in, void* const* h_out, int count, void* stream) {
+  if (!pl || !h_in || !h_out || count < 1) return fail(EFFT_ERR_INVALID_ARG, "NULL argument or count < 1");
+  for (int k = 0; k < count; ++k)
+    if (!h_in[k] || !h_out[k]) return fail(EFFT_ERR_INVALID_ARG, "NULL host buffer %d", k);
+  CUDA_TRY(cudaSetDevice(pl->device));
+  const size_t bytes = (size_t)pl->n * pl->elem;
+  size_t free_b = 0, total_b = 0;
+  CUDA_TRY(cudaMemGetInfo(&free_b, &total_b));
+  if (count == 1 || free_b < 4 * bytes + (1ull << 30)) {  // no room for two in/out pairs: one at a time
+    for (int k = 0; k < count; ++k) {
+      int rc = efft_execute_host(pl, h_in[k], h_out[k], stream);
+      if (rc != EFFT_OK) return rc;
+    }
+    return EFFT_OK;
+  }
+  // Two device in/out pairs; transform k+1's H2D (copy stream) overlaps
+  // transform k's passes and D2H (the caller's stream): the two PCIe
+  // directions run concurrently.
+  void* din[2] = {nullptr, nullptr};
+  void* dout[2] = {nullptr, nullptr};
+  cudaStream_t s = (cudaStream_t)stream, cs = nullptr;
+  cudaEvent_t in_ready[2] = {nullptr, nullptr}, buf_free[2] = {nullptr, nullptr};
+  int rc = EFFT_OK;
+  auto cleanup = [&]() {
+    for (int b = 0; b < 2; ++b) {
+      if (din[b]) cudaFree(din[b]);
+      if (dout[b]) cudaFree(dout[b]);
+      if (in_ready[b]) cudaEventDestroy(in_ready[b]);
+      if (buf_free[b]) cudaEventDestroy(buf_free[b]);
+    }
+    if (cs) cudaStreamDestroy(cs);
+  };
+  for (int b = 0; b < 2 && rc == EFFT_OK; ++b) {
+    if (cudaMalloc(&din[b], bytes) != cudaSuccess || cudaMalloc(&dout[b], bytes) != cudaSuccess ||
+        cudaEventCreateWithFlags(&in_ready[b], cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&buf_free[b], cudaEventDisableTiming) != cudaSuccess) {
+      cudaGetLastError();
+      rc = fail(EFFT_ERR_ALLOC, "double-buffered host execution (%zu bytes x 4)", bytes);
+    }
+  }
+  if (rc == EFFT_OK && cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking) != cudaSuccess)
+    rc = fail(EFFT_ERR_CUDA, "copy stream");
+  if (rc == EFFT_OK && cudaEventRecord(buf_free[0], s) != cudaSuccess) rc = fail(EFFT_ERR_CUDA, "event");
+  if (rc == EFFT_OK && cudaEventRecord(buf_free[1], s) != cudaSuccess) rc = fail(EFFT_ERR_CUDA, "event");
+  for (int k = 0; k < count && rc == EFFT_OK; ++k) {
+    const int b = k & 1;
+    if (cudaStreamWaitEvent(cs, buf_free[b], 0) != cudaSuccess ||
+        cudaMemcpyAsync(din[b], h_in[k], bytes, cudaMemcpyHostToDevice, cs) != cudaSuccess ||
+        cudaEventRecord(in_ready[b], cs) != cudaSuccess || cudaStreamWaitEvent(s, in_ready[b], 0) != cudaSuccess) {
+      rc = fail(EFFT_ERR_CUDA, "batch copy-in %d: %s", k, cudaGetErrorString(cudaGetLastError()));
+      break;
+    }
+    rc = efft_execute(pl, din[b], dout[b], stream);
+    if (rc != EFFT_OK) break;
+    if (cudaMemcpyAsync(h_out[k], dout[b], bytes, cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+        cudaEventRecord(buf_free[b], s) != cudaSuccess) {
+      rc = fail(EFFT_ERR_CUDA, "batch copy-out %d: %s", k, cudaGetErrorString(cudaGetLastError()));
+      break;
+    }
+  }
+  if (cudaStreamSynchronize(s) != cudaSuccess && rc == EFFT_OK) rc = fail(EFFT_ERR_CUDA, "batch sync");
+  if (cs && cudaStreamSynchronize(cs) != cudaSuccess && rc == EFFT_OK) rc = fail(EFFT_ERR_CUDA, "batch sync");
+  cleanup();
+  return rc;
+}
+
 int efft_release_host_buffers(int device) {
   if (device < 0 || device >= kMaxDevices) return fail(EFFT_ERR_INVALID_ARG, "device %d", device);
   HostPool& hp = host_pool(device);

@@ -161,6 +161,21 @@ class TestHandle:
             h.data[5] = 0
             h.run()  # flag cleared
 
+    def test_host_batch_entry_matches_single_calls(self):
+        """efft_execute_host_batch (pipelined H2D / passes / D2H) == one call per input."""
+        from paper_1409_5757_b200 import _native
+
+        n = 1 << 22
+        xs = [random_c(n, seed=s).astype(np.complex64) for s in (1, 2, 3)]
+        p = _native.NativePlan(n, _native.EFFT_C64, -1, 0)
+        ins = [torch.from_numpy(x).pin_memory() for x in xs]
+        outs = [torch.empty_like(t).pin_memory() for t in ins]
+        p.execute_host_batch([t.data_ptr() for t in ins], [t.data_ptr() for t in outs], 0)
+        for x, o in zip(xs, outs):
+            one = np.empty_like(x)
+            p.execute_host(x.ctypes.data, one.ctypes.data, 0)
+            assert np.array_equal(o.numpy(), one)
+
     def test_host_buffer_entry_matches_device_entry(self):
         n = 2 ** 18
         x = random_c(n, seed=3)
