@@ -1,5 +1,6 @@
 // lean.cu -- lean staged passes for the large DFTs: complex64 and complex128,
-// N = 2^k (2^26 <= N <= 2^32) and N = 3 * 2^k (3 * 2^24 <= N <= 3 * 2^30).
+// N = 2^k (2^26 <= N <= 2^32; complex64 from 2^24) and N = 3 * 2^k
+// (3 * 2^24 <= N <= 3 * 2^30).
 //
 // Same algorithm as the generic staged pass (efft_kernels.cuh: the four-step
 // form of the reference's scatter -> leaves -> merges, scatter.py:31-57,
@@ -740,6 +741,7 @@ static void* pick(int ra, int rb, bool t1) {
 }
 static void* pick_pair(int rb, bool t1) {
   switch (rb) {
+    case 16: return t1 ? (void*)lean_pair<16, true> : (void*)lean_pair<16, false>;
     case 32: return t1 ? (void*)lean_pair<32, true> : (void*)lean_pair<32, false>;
     case 64: return t1 ? (void*)lean_pair<64, true> : (void*)lean_pair<64, false>;
     case 128: return t1 ? (void*)lean_pair<128, true> : (void*)lean_pair<128, false>;
@@ -768,7 +770,10 @@ bool plan(int64_t n, int c128, int inverse, bool scale_inverse, bool check_finit
   const int ra2 = m == 3 ? 192 : 256;
   const int lbs = m == 3 ? t - 14 : t - 16;
   const int lb1 = (lbs + 1) / 2, lb2 = lbs - lb1;
-  if (lb1 < 5 || lb1 > 8 || lb2 < 5 || lb2 > 8) return false;
+  // rho_b >= 32 (QB >= 2) in general; the paired complex64 kernel also runs
+  // rho_b = 16 (QB = 1: the B stage is one 16-point DFT), down to N = 2^24
+  const int lbmin = (!c128 && m == 1) ? 4 : 5;
+  if (lb1 < lbmin || lb1 > 8 || lb2 < lbmin || lb2 > 8) return false;
   const int64_t R1 = int64_t(256) << lb1, R2 = (int64_t)ra2 << lb2;
   const int F = c128 ? 8 : 16, NT = 16 * F;
   const size_t elem = c128 ? 16 : 8;

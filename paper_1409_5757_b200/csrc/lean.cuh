@@ -2,8 +2,8 @@
 //
 // The lean path runs the large power-of-two transforms (complex64 and
 // complex128, N = R1 * R2 with R = rho_a * rho_b, rho_a = 256 (or 192 in pass 1
-// for N = 3 * 2^k), rho_b in {32, 64, 128, 256}: 2^26 <= N <= 2^32 and
-// 3 * 2^24 <= N <= 3 * 2^30) as two staged passes of one persistent kernel each:
+// for N = 3 * 2^k), rho_b in {32, 64, 128, 256} (also 16 for complex64):
+// 2^26 (2^24 for complex64) <= N <= 2^32 and 3 * 2^24 <= N <= 3 * 2^30) as two staged passes of one persistent kernel each:
 //   pass 1: x[j2 + R2*j1] -> y[k1 + R1*j2] (DFT over j1, the four-step twiddle
 //           W_N^(j2*k1) fused into the store, the j2 <-> k1 transpose fused
 //           into sub-stage A's register exchange)

@@ -57,6 +57,19 @@ def test_lean_forward_inverse_vs_oracle(lg, dtype):
     assert oracle.rel_l2(w.cpu().numpy(), oracle.transform(x, direction=1)) <= tol(n, dtype)
 
 
+@pytest.mark.parametrize("lg", [24, 25])
+def test_lean_complex64_rho_b_16_vs_oracle(lg):
+    """complex64 from 2^24: rho_b = 16 (the B stage is one 16-point DFT)."""
+    n = 1 << lg
+    x = random_c(n, seed=lg + 100)
+    xd = torch.from_numpy(x.astype(np.complex64)).cuda()
+    p, y = run(xd, "complex64")
+    assert "rho_b=16" in p.describe()
+    assert oracle.rel_l2(y.cpu().numpy(), oracle.transform(x)) <= tol(n, "complex64")
+    _, z = run(y, "complex64", direction=1)
+    assert oracle.rel_l2(z.cpu().numpy(), x) <= 2 * tol(n, "complex64")
+
+
 @pytest.mark.parametrize("dtype", ["complex64", "complex128"])
 @pytest.mark.parametrize("n", [3 << 24, 3 << 25])
 def test_lean_radix3_family_vs_oracle(n, dtype):
