@@ -16,7 +16,7 @@ include/efft_b200.h); this package is the host-side mirror of the reference
 interface.  There is no CPU fallback.
 """
 
-from . import errors
+from . import errors, outofcore
 from .core import (
     PermSpectrum,
     TransformHandle,
@@ -42,6 +42,7 @@ __all__ = [
     "data_view",
     "efficiency",
     "errors",
+    "outofcore",
     "flops_model",
     "handle_create",
     "plan_create",

@@ -200,15 +200,28 @@ def _read_raw(path: str, n: int, dtype: str) -> np.ndarray:
     return np.fromfile(path, dtype=npdt, count=n)
 
 
-def cmd_transform(input_path, output_path, n, splits, dtype, device, test_mode=False) -> int:
-    """Raw little-endian file in, spectrum out (float32: packed PERM; complex: natural order)."""
+def cmd_transform(input_path, output_path, n, splits, dtype, device, test_mode=False, device_bytes=0) -> int:
+    """Raw little-endian file in, spectrum out (float32: packed PERM; complex: natural order).
+    With --device-bytes (complex dtypes) the transform streams the host array
+    through that much device memory (outofcore.py)."""
+    import time
+
     try:
         x = _read_raw(input_path, n, dtype)
+        if device_bytes and dtype != "float32":
+            from . import outofcore
+
+            t0 = time.perf_counter()
+            y = outofcore.transform(x, device=device, device_bytes=device_bytes)
+            wall = time.perf_counter() - t0
+            y.tofile(output_path)
+            print(CSV_HEADER)
+            print(RunMetrics.from_timing(n, splits, 1, wall, dtype=dtype).csv_row())
+            return 0
         plan = plan_create(n, splits, 1, test_mode=test_mode, dtype=dtype, device=device)
     except (OSError, ValueError, EfftError) as exc:
         print(f"error: {exc}", file=sys.stderr)
         return 1
-    import time
 
     with handle_create(plan) as h:
         h.data[:] = x
@@ -239,6 +252,8 @@ def build_parser() -> argparse.ArgumentParser:
     p.add_argument("--splits", type=int, required=True)
     p.add_argument("--input", required=True)
     p.add_argument("--output", required=True)
+    p.add_argument("--device-bytes", type=int, default=0,
+                   help="stream the array through this much device memory (complex dtypes; out of core)")
     p = sub.add_parser("scan", help="bench rows over a list of split counts")
     common(p, repeats=True)
     p.add_argument("--splits", required=True, help="comma-separated split counts")
@@ -261,7 +276,8 @@ def main(argv=None) -> int:
         print(f"error: {exc}", file=sys.stderr)
         return 1
     if args.cmd == "transform":
-        return cmd_transform(args.input, args.output, n, args.splits, args.dtype, args.device, args.test_mode)
+        return cmd_transform(args.input, args.output, n, args.splits, args.dtype, args.device, args.test_mode,
+                             args.device_bytes)
     if args.cmd == "scan":
         return cmd_scan(n, parse_int_list(args.splits), args.repeats, args.dtype, args.device, args.test_mode)
     if args.cmd == "check":

@@ -51,3 +51,15 @@ def test_transform_file_roundtrip(tmp_path, capsys):
                      "--input", str(src), "--output", str(dst)]) == 0
     y = np.fromfile(dst, dtype=np.complex128)
     assert np.linalg.norm(y - np.fft.fft(x)) / np.linalg.norm(np.fft.fft(x)) < 1e-12
+
+
+def test_transform_out_of_core_option(tmp_path, capsys):
+    n = 1 << 20
+    x = (np.random.default_rng(7).standard_normal(n) + 1j * np.random.default_rng(8).standard_normal(n))
+    src, dst = tmp_path / "in.bin", tmp_path / "out.bin"
+    x.astype(np.complex128).tofile(src)
+    assert cli.main(["transform", "--size", "2^20", "--splits", "2", "--dtype", "complex128",
+                     "--input", str(src), "--output", str(dst), "--device-bytes", str(1 << 20)]) == 0
+    y = np.fromfile(dst, dtype=np.complex128)
+    ref = np.fft.fft(x)
+    assert np.linalg.norm(y - ref) / np.linalg.norm(ref) < 1e-12
