@@ -68,7 +68,7 @@ int64_t efo_bitrev(int64_t j, int bits) {
   return r;
 }
 
-/* Size decomposition n = M * 2^t with M odd in {1, 3}. */
+/* Size decomposition n = M * 2^t with M odd in {1, 3, 5, 7}. */
 static int efo_factor(int64_t n, int64_t *M, int *t) {
   if (n < 1) return EFO_EINVAL;
   int tt = 0;
@@ -76,7 +76,7 @@ static int efo_factor(int64_t n, int64_t *M, int *t) {
     n >>= 1;
     ++tt;
   }
-  if (n != 1 && n != 3) return EFO_EINVAL;
+  if (n != 1 && n != 3 && n != 5 && n != 7) return EFO_EINVAL;
   *M = n;
   *t = tt;
   return EFO_OK;
@@ -131,7 +131,7 @@ static void efo_set_threads(int threads) {
    * oracle.py:43-51. */                                                        \
   static void efo_small_dft_##SUF(REAL *v, int64_t M) {                         \
     if (M == 1) return;                                                         \
-    double tmp[2 * 3];                                                          \
+    double tmp[2 * 7]; /* M <= 7 */                                             \
     for (int64_t k = 0; k < M; ++k) {                                           \
       double ar = 0, ai = 0;                                                    \
       for (int64_t n = 0; n < M; ++n) {                                         \

@@ -32,6 +32,7 @@
 #include <type_traits>
 
 #include "w192_table.cuh"
+#include "w320_table.cuh"
 
 namespace efft {
 
@@ -288,10 +289,33 @@ __device__ __forceinline__ int32_t ld_acquire(const int32_t* ctr) {
 // order generic-proxy writes observed through an acquire before async-proxy reads
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
 
-// b * W_N^K, N | 192, K compile-time: trivial roots become sign swaps, the
-// rest immediate-operand complex multiplies.
+// b * W_N^K, N | 192 or N | 320, K compile-time: trivial roots become sign
+// swaps, the rest immediate-operand complex multiplies.
+template <typename R, int N, int K>
+__device__ __forceinline__ typename CT<R>::V twk5(typename CT<R>::V b) {
+  static_assert(320 % N == 0, "register DFT size must divide 192 or 320");
+  constexpr int Q = (K % N) * (320 / N);
+  if constexpr (Q == 0) {
+    return b;
+  } else if constexpr (Q == 80) {
+    return mk(b.y, -b.x);  // -i
+  } else if constexpr (Q == 160) {
+    return mk(-b.x, -b.y);
+  } else if constexpr (Q == 240) {
+    return mk(-b.y, b.x);  // +i
+  } else {
+    constexpr R wr = (R)W320::v[Q][0], wi = (R)W320::v[Q][1];
+    if constexpr (sizeof(R) == 4)
+      return fma2(make_float2(b.y, b.y), make_float2(-wi, wr), mul2(make_float2(b.x, b.x), make_float2(wr, wi)));
+    else
+      return mk(fma(b.x, wr, -b.y * wi), fma(b.x, wi, b.y * wr));
+  }
+}
 template <typename R, int N, int K>
 __device__ __forceinline__ typename CT<R>::V twk(typename CT<R>::V b) {
+  if constexpr (192 % N != 0) {
+    return twk5<R, N, K>(b);
+  } else {
   static_assert(192 % N == 0, "register DFT size must divide 192");
   constexpr int Q = (K % N) * (192 / N);
   if constexpr (Q == 0) {
@@ -323,6 +347,7 @@ __device__ __forceinline__ typename CT<R>::V twk(typename CT<R>::V b) {
     else
       return mk(fma(b.x, wr, -b.y * wi), fma(b.x, wi, b.y * wr));
   }
+  }
 }
 
 // ----------------------------------------------------------------------------
@@ -353,11 +378,34 @@ template <typename V> __device__ __forceinline__ void dft3(V* a) {
   a[2] = csub(t2, t3);
 }
 
+// 5-point DFT (forward): pairs (1,4), (2,3) with c_k = cos(2 pi k/5),
+// s_k = sin(2 pi k/5); X_1,4 = a0 + c1 t1 + c2 t2 -/+ i (s1 d1 + s2 d2),
+// X_2,3 = a0 + c2 t1 + c1 t2 -/+ i (s2 d1 - s1 d2).
+template <typename V> __device__ __forceinline__ void dft5(V* a) {
+  using R = decltype(a[0].x);
+  constexpr R c1 = R(0.30901699437494742410229341718281905886);
+  constexpr R c2 = R(-0.80901699437494742410229341718281905886);
+  constexpr R s1 = R(0.95105651629515357211643933337938214340);
+  constexpr R s2 = R(0.58778525229247312916870595463907276860);
+  const V t1 = cadd(a[1], a[4]), d1 = csub(a[1], a[4]);
+  const V t2 = cadd(a[2], a[3]), d2 = csub(a[2], a[3]);
+  const V a0 = a[0];
+  const V u1 = mk(a0.x + c1 * t1.x + c2 * t2.x, a0.y + c1 * t1.y + c2 * t2.y);
+  const V u2 = mk(a0.x + c2 * t1.x + c1 * t2.x, a0.y + c2 * t1.y + c1 * t2.y);
+  const V w1 = mk(s1 * d1.x + s2 * d2.x, s1 * d1.y + s2 * d2.y);
+  const V w2 = mk(s2 * d1.x - s1 * d2.x, s2 * d1.y - s1 * d2.y);
+  a[0] = cadd(a0, cadd(t1, t2));
+  a[1] = mk(u1.x + w1.y, u1.y - w1.x);  // u1 - i w1
+  a[4] = mk(u1.x - w1.y, u1.y + w1.x);  // u1 + i w1
+  a[2] = mk(u2.x + w2.y, u2.y - w2.x);
+  a[3] = mk(u2.x - w2.y, u2.y + w2.x);
+}
+
 // In-place decimation-in-frequency network over a contiguous segment
-// [B, B+L) of v: radix r = 3 (if 3 | L), else 4, else 2; twiddles
+// [B, B+L) of v: radix r = 3 (if 3 | L), else 5, else 4, else 2; twiddles
 // W_L^(j*k) are compile-time constants.  Output X[k] ends at v[dif_pos<N>(k)]
 // (mixed-radix digit reversal; free renaming, no register copies).
-constexpr int dif_radix_rt(int L) { return (L % 3 == 0) ? 3 : (L % 4 == 0) ? 4 : 2; }
+constexpr int dif_radix_rt(int L) { return (L % 3 == 0) ? 3 : (L % 5 == 0) ? 5 : (L % 4 == 0) ? 4 : 2; }
 constexpr int dif_pos(int L, int k) {
   // position of output k of an L-point in-place DIF transform
   int pos = 0;
@@ -384,6 +432,7 @@ __device__ __forceinline__ void dif_segment(typename CT<R>::V* v) {
       if constexpr (r == 2) dft2(a);
       if constexpr (r == 3) dft3(a);
       if constexpr (r == 4) dft4(a);
+      if constexpr (r == 5) dft5(a);
       cfor<0, r>([&](auto T) {
         constexpr int k = decltype(T)::value;
         v[B + j + k * q] = twk<R, L, j * k>(a[k]);
@@ -434,15 +483,22 @@ struct PassArgs {
   alignas(64) CUtensorMap tmB;
 };
 
-// e = A*C mod M for M = 2^k or 3*2^k (A, C >= 0), exact.
+// e = A*C mod M for M = m*2^k, m in {1, 3, 5} (A, C >= 0), exact: the low k
+// bits come from the 64-bit product, the residue mod m by CRT.
 __device__ __forceinline__ int64_t mulmod(int64_t A, int64_t C, int64_t M) {
   const uint64_t lo = (uint64_t)A * (uint64_t)C;  // exact mod 2^64
   if ((M & (M - 1)) == 0) return (int64_t)(lo & (uint64_t)(M - 1));
-  const int k = __ffsll(M) - 1;  // M = 3 * 2^k
+  const int k = __ffsll(M) - 1;  // M = m * 2^k
+  const int m = (int)(M >> k);
   const uint64_t p2 = lo & ((1ull << k) - 1);
-  const int m3 = (int)(((A % 3) * (C % 3)) % 3);
-  const int inv = (k & 1) ? 2 : 1;  // (2^k)^-1 mod 3
-  const int y = (((m3 - (int)(p2 % 3)) % 3 + 3) * inv) % 3;
+  const int mm = (int)(((A % m) * (C % m)) % m);
+  int pw = 1;  // 2^k mod m, then its inverse
+  for (int i = 0; i < (k & 3); ++i) pw = (2 * pw) % m;
+  if (m == 3 && (k & 1)) pw = 2;
+  if (m == 3 && !(k & 1)) pw = 1;
+  int inv = 1;
+  while ((inv * pw) % m != 1) ++inv;
+  const int y = (((mm - (int)(p2 % m)) % m + m) * inv) % m;
   return (int64_t)(p2 + ((uint64_t)y << k));
 }
 
@@ -462,11 +518,11 @@ struct StagePlan {
 };
 constexpr StagePlan make_stage_plan(int rho, int e) {
   StagePlan p{0, {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0}};
-  const int cand[9] = {32, 24, 16, 12, 8, 6, 4, 3, 2};
+  const int cand[12] = {32, 24, 20, 16, 12, 10, 8, 6, 5, 4, 3, 2};
   int rem = rho;
   while (rem > 1) {
     int pick = 0;
-    for (int i = 0; i < 9; ++i)
+    for (int i = 0; i < 12; ++i)
       if (rem % cand[i] == 0 && e % cand[i] == 0) {
         pick = cand[i];
         break;

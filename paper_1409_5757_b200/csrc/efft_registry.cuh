@@ -13,17 +13,22 @@ struct KernelInfo {
   int stages_a[12], nst_a;
   int stages_b[12], nst_b;
   int ws;    // warp-specialised TMA kernel (needs tensor maps)
-  int tpts;  // D * RHO of the tiles (points per column group per task)
+  int tpts;    // D * RHO of the A tiles (points per column group per task)
+  int tpts_b;  // D * RHO of the B tiles
 };
 
 // Power-of-two tiles hold D*RHO = 512 points per column group, radix-3 tiles
-// 384; 256 threads; F columns of 128 bytes.
+// 384, radix-5 tiles 320 (one complex element per lane access: EV = 10 / 20
+// takes radix-10/5/20 stages); 256 threads; F columns of 128 bytes.
 template <typename R, int RHO, bool MASK> using PT = Tile<R, RHO, 512 / RHO, 256, MASK, CT<R>::VEC>;
 template <typename R, int RHO, bool MASK> using T3 = Tile<R, RHO, 384 / RHO, 256, MASK, CT<R>::VEC>;
+template <typename R, int RHO, bool MASK> using T5 = Tile<R, RHO, 320 / RHO, 256, MASK, 1>;
+// points per column group of a tile whose radix is RHO
+constexpr int tile_points(int rho) { return rho % 3 == 0 ? 384 : rho % 5 == 0 ? 320 : 512; }
 // Consumer tiles of the warp-specialised staged kernel: 256 consumer threads
 // after the producer warp (TOFF 32), named barrier 1, one complex element per
 // lane access.
-template <typename R, int RHO> using ST = Tile<R, RHO, (RHO % 3 ? 512 : 384) / RHO, 256, false, 1, 32, 1, true>;
+template <typename R, int RHO> using ST = Tile<R, RHO, tile_points(RHO) / RHO, 256, false, 1, 32, 1, true>;
 
 template <typename R, class TA, class TB, bool WS = false, int NBUF = 2>
 KernelInfo make_info() {
@@ -48,6 +53,7 @@ KernelInfo make_info() {
   for (int i = 0; i < TA::NST; ++i) k.stages_a[i] = TA::PL.sig[i];
   if constexpr (TB::RHO > 0) {
     k.rho_b = TB::RHO;
+    k.tpts_b = TB::D * TB::RHO;
     k.d_b = TB::D;
     k.e_b = TB::E;
     k.nst_b = TB::NST;

@@ -41,7 +41,9 @@ def gpu_transform(x, dtype, direction=-1):
 
 
 SIZES = [2, 4, 8, 16, 32, 64, 128, 256, 512, 1024, 3, 6, 12, 24, 48, 96, 192, 384, 768, 3 * 1024,
-         4096, 2 ** 14, 3 * 2 ** 14, 2 ** 16, 2 ** 18, 2 ** 19, 2 ** 20, 3 * 2 ** 19, 2 ** 21]
+         4096, 2 ** 14, 3 * 2 ** 14, 2 ** 16, 2 ** 18, 2 ** 19, 2 ** 20, 3 * 2 ** 19, 2 ** 21,
+         # radix-5 family: direct 5..320, two direct passes, staged rho_a = 320
+         5, 10, 40, 160, 320, 640, 5 * 2 ** 10, 5 * 2 ** 14, 5 * 2 ** 16, 5 * 2 ** 19]
 
 
 @pytest.mark.parametrize("dtype", ["complex64", "complex128"])
@@ -282,8 +284,8 @@ def test_c5_2p32_complex128_roundtrip_and_spots():
         pytest.skip("needs ~130 GiB of device memory")
     import psutil
 
-    if psutil.virtual_memory().available < 2 * n * 16 + (8 << 30):
-        pytest.skip("needs ~140 GB of host memory for the host-side checks")
+    if psutil.virtual_memory().available < n * 16 + (16 << 30):
+        pytest.skip("needs ~80 GB of host memory for the host-side checks")
     seed = workloads.seed_for("c5")
     x = workloads.make_input(n, "complex128", "uniform", seed)
     xh = x.cpu().numpy()
@@ -306,6 +308,11 @@ def test_c5_2p32_complex128_roundtrip_and_spots():
     inv.execute(y.data_ptr(), x.data_ptr(), s)  # overwrite x; xh holds the original
     torch.cuda.synchronize()
     del y
-    z = x.cpu().numpy()
-    rt = float(np.linalg.norm(z - xh) / np.linalg.norm(xh))
+    # round-trip error chunk by chunk on the device (no second 64 GiB host copy)
+    num = den = 0.0
+    for i in range(0, n, 1 << 28):
+        xc = torch.from_numpy(xh[i:i + (1 << 28)]).cuda()
+        num += torch.view_as_real(x[i:i + (1 << 28)] - xc).pow(2).sum().item()
+        den += torch.view_as_real(xc).pow(2).sum().item()
+    rt = math.sqrt(num / den)
     assert rt <= 2 * tol(n, "complex128")

@@ -108,7 +108,7 @@ def test_c1_spot_checks_vs_reference_naive_dft_at():
 
 
 # ---- self-consistency -------------------------------------------------------
-@pytest.mark.parametrize("n", [8, 96, 1024, 3 * 2 ** 12, 2 ** 16])
+@pytest.mark.parametrize("n", [8, 96, 1024, 3 * 2 ** 12, 2 ** 16, 5, 40, 5 * 2 ** 12, 7 * 2 ** 10])
 def test_roundtrip_and_numpy(n):
     x = random_c(n, seed=n)
     y = oracle.transform(x)

@@ -9,8 +9,9 @@ def test_split_balanced_and_factor3_first():
     assert outofcore.split(1 << 30) == (1 << 15, 1 << 15)
     assert outofcore.split(1 << 31) == (1 << 15, 1 << 16)
     assert outofcore.split(3 << 28) == (3 << 14, 1 << 14)
+    assert outofcore.split(5 << 20) == (5 << 10, 1 << 10)
     with pytest.raises(BinsizeNotPowerOfTwo):
-        outofcore.split(5 << 20)
+        outofcore.split(7 << 20)
     with pytest.raises(BinsizeNotPowerOfTwo):
         outofcore.split(1 << 36)
 
