@@ -39,7 +39,7 @@ extern "C" {
 #define EFFT_ERR_INVALID_ARG 1    /* ValueError                core.py:78-85        */
 #define EFFT_ERR_SPLITS_TOO_LARGE 2 /* SplitsTooLarge          core.py:87-89        */
 #define EFFT_ERR_SIZE_CONSTRAINT 3 /* SizeConstraintViolation core.py:90-94        */
-#define EFFT_ERR_UNSUPPORTED_SIZE 4 /* BinsizeNotPowerOfTwo    core.py:95-100 (here: N not M*2^t, M in {1,3,5}) */
+#define EFFT_ERR_UNSUPPORTED_SIZE 4 /* BinsizeNotPowerOfTwo    core.py:95-100 (here: N not M*2^t, M in {1,3,5,7}) */
 #define EFFT_ERR_ALLOC 5          /* AllocationFailure         memory.py:51-54      */
 #define EFFT_ERR_SIZE_MISMATCH 6  /* SizeMismatch              scatter.py:34-37     */
 #define EFFT_ERR_NONFINITE 7      /* ValueError (non-finite)   scatter.py:38-39     */

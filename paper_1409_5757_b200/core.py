@@ -7,7 +7,7 @@ Mirrors the reference's public surface (reference pkg/src/efft/core.py):
   keywords ``dtype`` ("float32" = the reference's real-input PERM layout,
   "complex64", "complex128"), ``direction`` (-1 forward unnormalised, +1
   inverse scaled by 1/N) and ``device``.  Complex plans accept n = M * 2^t with
-  M in {1, 3, 5} (the paper's M x 2^s sizes); the real path keeps
+  M in {1, 3, 5, 7} (the paper's M x 2^s sizes); the real path keeps
   the reference's power-of-two bin rule byte for byte.
 * ``TransformHandle`` owns the device buffers (torch CUDA tensors), pinned host
   views ``data`` (writable, preserved across runs, core.py:146-149) and
@@ -45,12 +45,12 @@ def _is_pow2(v: int) -> bool:
 
 
 def _is_m_pow2(v: int) -> bool:
-    """v = M * 2^k with M in {1, 3, 5}."""
+    """v = M * 2^k with M in {1, 3, 5, 7}."""
     if v < 1:
         return False
     while v % 2 == 0:
         v //= 2
-    return v in (1, 3, 5)
+    return v in (1, 3, 5, 7)
 
 
 def build_scatter_index(splits: int) -> np.ndarray:
@@ -138,7 +138,7 @@ def plan_create(
     else:
         if binsize * bins != n or not _is_m_pow2(binsize) or n < 2:
             raise BinsizeNotPowerOfTwo(
-                f"bin size {n}/{bins} must be M*2^k with M in (1, 3, 5) for complex transforms"
+                f"bin size {n}/{bins} must be M*2^k with M in (1, 3, 5, 7) for complex transforms"
             )
     return TransformPlan(
         n=n, splits=splits, bins=bins, binsize=binsize,

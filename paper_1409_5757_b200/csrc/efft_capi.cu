@@ -1,7 +1,7 @@
 // efft_capi.cu -- planner, executor and the C ABI (include/efft_b200.h).
 //
 // Planner (reference counterpart: plan_create, core.py:63-111).  N = M * 2^t,
-// M in {1, 3, 5}, is split into at most two Stockham passes N = R1 * R2 (the
+// M in {1, 3, 5, 7}, is split into at most two Stockham passes N = R1 * R2 (the
 // four-step form of the reference's scatter -> leaves -> merges).  A pass whose
 // radix fits one tile (<= 512 points, <= 384 with the factor 3) is "direct";
 // a larger one is "staged" as R = rho_a * rho_b through the L2 staging ring.
@@ -147,7 +147,7 @@ bool factor(int64_t n, int* M, int* t) {
     n >>= 1;
     ++tt;
   }
-  if (n != 1 && n != 3 && n != 5) return false;
+  if (n != 1 && n != 3 && n != 5 && n != 7) return false;
   *M = (int)n;
   *t = tt;
   return true;
@@ -169,8 +169,8 @@ bool get_staged(int dtype, int ra, int rb, KernelInfo* k) {
 // Decide direct vs staged and the sub-radices of one pass of radix R.
 bool pick_pass(int dtype, int64_t R, PassPlan* pp) {
   pp->radix = R;
-  const bool has3 = (R % 3) == 0, has5 = (R % 5) == 0;
-  const int64_t dmax = has3 ? 384 : has5 ? 320 : 512;
+  const bool has3 = (R % 3) == 0, has5 = (R % 5) == 0, has7 = (R % 7) == 0;
+  const int64_t dmax = has3 ? 384 : has5 ? 320 : has7 ? 448 : 512;
   if (R <= dmax) {
     pp->staged = false;
     pp->rho_a = R;
@@ -178,7 +178,7 @@ bool pick_pass(int dtype, int64_t R, PassPlan* pp) {
     return get_direct(dtype, (int)R, &pp->k);
   }
   pp->staged = true;
-  pp->rho_a = has3 ? 384 : has5 ? 320 : 256;
+  pp->rho_a = has3 ? 384 : has5 ? 320 : has7 ? 448 : 256;
   pp->rho_b = R / pp->rho_a;
   if (pp->rho_b * pp->rho_a != R || pp->rho_b > 512) return false;
   bool ok;
@@ -388,10 +388,10 @@ int build_plan(efft_plan_s* pl) {
   int M, t;
   if (pl->columns) {
     if (!factor(pl->col_len, &M, &t) || pl->col_len < 2)
-      return fail(EFFT_ERR_UNSUPPORTED_SIZE, "len=%lld is not M*2^t with M in {1,3,5}", (long long)pl->col_len);
+      return fail(EFFT_ERR_UNSUPPORTED_SIZE, "len=%lld is not M*2^t with M in {1,3,5,7}", (long long)pl->col_len);
   } else if (!factor(pl->n, &M, &t) || pl->n < 2)
     return fail(EFFT_ERR_UNSUPPORTED_SIZE,
-                "n=%lld is not M*2^t with M in {1,3,5} and n >= 2", (long long)pl->n);
+                "n=%lld is not M*2^t with M in {1,3,5,7} and n >= 2", (long long)pl->n);
   const int dt = pl->dtype;
   if (!pl->columns && env_int("EFFT_LEAN", 1)) {
     int64_t stg = 0;
@@ -407,7 +407,7 @@ int build_plan(efft_plan_s* pl) {
     if (ecuda) return fail(EFFT_ERR_CUDA, "lean pass setup failed: %s", cudaGetErrorString(cudaGetLastError()));
   }
   int64_t R1, R2;
-  const int64_t dmax = M == 3 ? 384 : M == 5 ? 320 : 512;
+  const int64_t dmax = M == 3 ? 384 : M == 5 ? 320 : M == 7 ? 448 : 512;
   if (pl->columns) {
     pl->npass = 1;
     R1 = pl->col_len;

@@ -33,6 +33,7 @@
 
 #include "w192_table.cuh"
 #include "w320_table.cuh"
+#include "w448_table.cuh"
 
 namespace efft {
 
@@ -289,32 +290,36 @@ __device__ __forceinline__ int32_t ld_acquire(const int32_t* ctr) {
 // order generic-proxy writes observed through an acquire before async-proxy reads
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
 
-// b * W_N^K, N | 192 or N | 320, K compile-time: trivial roots become sign
+// b * W_N^K for N | T (T = 320 or 448, table W): trivial roots become sign
 // swaps, the rest immediate-operand complex multiplies.
-template <typename R, int N, int K>
-__device__ __forceinline__ typename CT<R>::V twk5(typename CT<R>::V b) {
-  static_assert(320 % N == 0, "register DFT size must divide 192 or 320");
-  constexpr int Q = (K % N) * (320 / N);
+template <typename R, int N, int K, int T, class W>
+__device__ __forceinline__ typename CT<R>::V twk_tab(typename CT<R>::V b) {
+  static_assert(T % N == 0, "register DFT size must divide the root table");
+  constexpr int Q = (K % N) * (T / N);
   if constexpr (Q == 0) {
     return b;
-  } else if constexpr (Q == 80) {
+  } else if constexpr (4 * Q == T) {
     return mk(b.y, -b.x);  // -i
-  } else if constexpr (Q == 160) {
+  } else if constexpr (2 * Q == T) {
     return mk(-b.x, -b.y);
-  } else if constexpr (Q == 240) {
+  } else if constexpr (4 * Q == 3 * T) {
     return mk(-b.y, b.x);  // +i
   } else {
-    constexpr R wr = (R)W320::v[Q][0], wi = (R)W320::v[Q][1];
+    constexpr R wr = (R)W::v[Q][0], wi = (R)W::v[Q][1];
     if constexpr (sizeof(R) == 4)
       return fma2(make_float2(b.y, b.y), make_float2(-wi, wr), mul2(make_float2(b.x, b.x), make_float2(wr, wi)));
     else
       return mk(fma(b.x, wr, -b.y * wi), fma(b.x, wi, b.y * wr));
   }
 }
+// b * W_N^K, N | 192, 320 or 448, K compile-time
 template <typename R, int N, int K>
 __device__ __forceinline__ typename CT<R>::V twk(typename CT<R>::V b) {
   if constexpr (192 % N != 0) {
-    return twk5<R, N, K>(b);
+    if constexpr (320 % N == 0)
+      return twk_tab<R, N, K, 320, W320>(b);
+    else
+      return twk_tab<R, N, K, 448, W448>(b);
   } else {
   static_assert(192 % N == 0, "register DFT size must divide 192");
   constexpr int Q = (K % N) * (192 / N);
@@ -401,11 +406,40 @@ template <typename V> __device__ __forceinline__ void dft5(V* a) {
   a[3] = mk(u2.x - w2.y, u2.y + w2.x);
 }
 
+// 7-point DFT (forward): X_k = a0 + sum_{j=1..3} [c_jk (a_j + a_7-j) - i s_jk (a_j - a_7-j)]
+// with c_m = cos(2 pi m/7), s_m = sin(2 pi m/7) (compile-time, from W_448).
+template <typename V> __device__ __forceinline__ void dft7(V* a) {
+  using R = decltype(a[0].x);
+  V t[4], d[4];
+  cfor<1, 4>([&](auto J) {
+    constexpr int j = decltype(J)::value;
+    t[j] = cadd(a[j], a[7 - j]);
+    d[j] = csub(a[j], a[7 - j]);
+  });
+  const V a0 = a[0];
+  a[0] = cadd(a0, cadd(t[1], cadd(t[2], t[3])));
+  cfor<1, 4>([&](auto K) {
+    constexpr int k = decltype(K)::value;
+    V u = a0, w = mk(R(0), R(0));
+    cfor<1, 4>([&](auto J) {
+      constexpr int j = decltype(J)::value;
+      constexpr int m = (j * k) % 7;
+      constexpr R c = (R)W448::v[64 * m][0], sn = (R)(-W448::v[64 * m][1]);
+      u = mk(u.x + c * t[j].x, u.y + c * t[j].y);
+      w = mk(w.x + sn * d[j].x, w.y + sn * d[j].y);
+    });
+    a[k] = mk(u.x + w.y, u.y - w.x);      // u - i w
+    a[7 - k] = mk(u.x - w.y, u.y + w.x);  // u + i w
+  });
+}
+
 // In-place decimation-in-frequency network over a contiguous segment
-// [B, B+L) of v: radix r = 3 (if 3 | L), else 5, else 4, else 2; twiddles
+// [B, B+L) of v: radix r = 3 (if 3 | L), else 5, else 7, else 4, else 2; twiddles
 // W_L^(j*k) are compile-time constants.  Output X[k] ends at v[dif_pos<N>(k)]
 // (mixed-radix digit reversal; free renaming, no register copies).
-constexpr int dif_radix_rt(int L) { return (L % 3 == 0) ? 3 : (L % 5 == 0) ? 5 : (L % 4 == 0) ? 4 : 2; }
+constexpr int dif_radix_rt(int L) {
+  return (L % 3 == 0) ? 3 : (L % 5 == 0) ? 5 : (L % 7 == 0) ? 7 : (L % 4 == 0) ? 4 : 2;
+}
 constexpr int dif_pos(int L, int k) {
   // position of output k of an L-point in-place DIF transform
   int pos = 0;
@@ -433,6 +467,7 @@ __device__ __forceinline__ void dif_segment(typename CT<R>::V* v) {
       if constexpr (r == 3) dft3(a);
       if constexpr (r == 4) dft4(a);
       if constexpr (r == 5) dft5(a);
+      if constexpr (r == 7) dft7(a);
       cfor<0, r>([&](auto T) {
         constexpr int k = decltype(T)::value;
         v[B + j + k * q] = twk<R, L, j * k>(a[k]);
@@ -483,7 +518,7 @@ struct PassArgs {
   alignas(64) CUtensorMap tmB;
 };
 
-// e = A*C mod M for M = m*2^k, m in {1, 3, 5} (A, C >= 0), exact: the low k
+// e = A*C mod M for M = m*2^k, m in {1, 3, 5, 7} (A, C >= 0), exact: the low k
 // bits come from the 64-bit product, the residue mod m by CRT.
 __device__ __forceinline__ int64_t mulmod(int64_t A, int64_t C, int64_t M) {
   const uint64_t lo = (uint64_t)A * (uint64_t)C;  // exact mod 2^64
@@ -493,9 +528,7 @@ __device__ __forceinline__ int64_t mulmod(int64_t A, int64_t C, int64_t M) {
   const uint64_t p2 = lo & ((1ull << k) - 1);
   const int mm = (int)(((A % m) * (C % m)) % m);
   int pw = 1;  // 2^k mod m, then its inverse
-  for (int i = 0; i < (k & 3); ++i) pw = (2 * pw) % m;
-  if (m == 3 && (k & 1)) pw = 2;
-  if (m == 3 && !(k & 1)) pw = 1;
+  for (int i = 0; i < k; ++i) pw = (2 * pw) % m;
   int inv = 1;
   while ((inv * pw) % m != 1) ++inv;
   const int y = (((mm - (int)(p2 % m)) % m + m) * inv) % m;
@@ -518,11 +551,11 @@ struct StagePlan {
 };
 constexpr StagePlan make_stage_plan(int rho, int e) {
   StagePlan p{0, {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0}};
-  const int cand[12] = {32, 24, 20, 16, 12, 10, 8, 6, 5, 4, 3, 2};
+  const int cand[15] = {32, 28, 24, 20, 16, 14, 12, 10, 8, 7, 6, 5, 4, 3, 2};
   int rem = rho;
   while (rem > 1) {
     int pick = 0;
-    for (int i = 0; i < 12; ++i)
+    for (int i = 0; i < 15; ++i)
       if (rem % cand[i] == 0 && e % cand[i] == 0) {
         pick = cand[i];
         break;

@@ -18,13 +18,17 @@ struct KernelInfo {
 };
 
 // Power-of-two tiles hold D*RHO = 512 points per column group, radix-3 tiles
-// 384, radix-5 tiles 320 (one complex element per lane access: EV = 10 / 20
-// takes radix-10/5/20 stages); 256 threads; F columns of 128 bytes.
+// 384, radix-5 tiles 320 and radix-7 tiles 448 (one complex element per lane
+// access: EV = 10..28 takes radix-20/14/10/7/5 stages); 256 threads; F columns
+// of 128 bytes.
 template <typename R, int RHO, bool MASK> using PT = Tile<R, RHO, 512 / RHO, 256, MASK, CT<R>::VEC>;
 template <typename R, int RHO, bool MASK> using T3 = Tile<R, RHO, 384 / RHO, 256, MASK, CT<R>::VEC>;
 template <typename R, int RHO, bool MASK> using T5 = Tile<R, RHO, 320 / RHO, 256, MASK, 1>;
+template <typename R, int RHO, bool MASK> using T7 = Tile<R, RHO, 448 / RHO, 256, MASK, 1>;
 // points per column group of a tile whose radix is RHO
-constexpr int tile_points(int rho) { return rho % 3 == 0 ? 384 : rho % 5 == 0 ? 320 : 512; }
+constexpr int tile_points(int rho) {
+  return rho % 3 == 0 ? 384 : rho % 5 == 0 ? 320 : rho % 7 == 0 ? 448 : 512;
+}
 // Consumer tiles of the warp-specialised staged kernel: 256 consumer threads
 // after the producer warp (TOFF 32), named barrier 1, one complex element per
 // lane access.

@@ -15,7 +15,7 @@ with bounded device buffers.  With N = N1 N2, x viewed as (N1 x N2) row-major
 Both steps use the library's column plans (efft_plan_create_columns) and the
 permutation kernel (efft_permute_swap01); the host side only reshuffles
 blocks.  Inverse = direction +1 with 1/N1 and 1/N2 scaling in the two column
-plans (1/N in total).  Sizes N = M 2^t, M in {1, 3, 5}, N1, N2 <= 2^17.
+plans (1/N in total).  Sizes N = M 2^t, M in {1, 3, 5, 7}, N1, N2 <= 2^17.
 """
 
 import math
@@ -36,8 +36,8 @@ def split(n: int):
     while m % 2 == 0:
         m //= 2
         t += 1
-    if m not in (1, 3, 5):
-        raise BinsizeNotPowerOfTwo(f"n={n} is not M*2^t with M in {{1, 3, 5}}")
+    if m not in (1, 3, 5, 7):
+        raise BinsizeNotPowerOfTwo(f"n={n} is not M*2^t with M in {{1, 3, 5, 7}}")
     t1 = t // 2
     n1, n2 = m << t1, 1 << (t - t1)
     if n1 > MAX_COLUMN_LEN or n2 > MAX_COLUMN_LEN:

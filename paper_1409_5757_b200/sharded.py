@@ -39,8 +39,8 @@ def split_sizes(n: int, world: int):
     while m % 2 == 0:
         m //= 2
         t += 1
-    if m not in (1, 3, 5) or world < 1 or world & (world - 1):
-        raise BinsizeNotPowerOfTwo(f"n={n} / world={world} not shardable (need n = M*2^t with M in {1, 3, 5}, G = 2^g)")
+    if m not in (1, 3, 5, 7) or world < 1 or world & (world - 1):
+        raise BinsizeNotPowerOfTwo(f"n={n} / world={world} not shardable (need n = M*2^t with M in {1, 3, 5, 7}, G = 2^g)")
     g = world.bit_length() - 1
     t1 = t // 2
     n1, n2 = m << t1, 1 << (t - t1)

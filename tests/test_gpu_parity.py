@@ -42,8 +42,10 @@ def gpu_transform(x, dtype, direction=-1):
 
 SIZES = [2, 4, 8, 16, 32, 64, 128, 256, 512, 1024, 3, 6, 12, 24, 48, 96, 192, 384, 768, 3 * 1024,
          4096, 2 ** 14, 3 * 2 ** 14, 2 ** 16, 2 ** 18, 2 ** 19, 2 ** 20, 3 * 2 ** 19, 2 ** 21,
-         # radix-5 family: direct 5..320, two direct passes, staged rho_a = 320
-         5, 10, 40, 160, 320, 640, 5 * 2 ** 10, 5 * 2 ** 14, 5 * 2 ** 16, 5 * 2 ** 19]
+         # radix-5 / radix-7 families: direct tiles, two direct
+         # passes, staged rho_a = 320 / 448
+         5, 10, 40, 160, 320, 640, 5 * 2 ** 10, 5 * 2 ** 14, 5 * 2 ** 16, 5 * 2 ** 19,
+         7, 28, 112, 448, 896, 7 * 2 ** 10, 7 * 2 ** 15, 7 * 2 ** 17, 7 * 2 ** 19]
 
 
 @pytest.mark.parametrize("dtype", ["complex64", "complex128"])

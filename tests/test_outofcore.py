@@ -10,8 +10,9 @@ def test_split_balanced_and_factor3_first():
     assert outofcore.split(1 << 31) == (1 << 15, 1 << 16)
     assert outofcore.split(3 << 28) == (3 << 14, 1 << 14)
     assert outofcore.split(5 << 20) == (5 << 10, 1 << 10)
+    assert outofcore.split(7 << 20) == (7 << 10, 1 << 10)
     with pytest.raises(BinsizeNotPowerOfTwo):
-        outofcore.split(7 << 20)
+        outofcore.split(9 << 20)
     with pytest.raises(BinsizeNotPowerOfTwo):
         outofcore.split(1 << 36)
 

@@ -32,10 +32,11 @@ class TestPlanCreate:
         # the paper's N = M x 2^s sizes; BASELINE config 4
         plan = plan_create(3 * 2 ** 28, 4, dtype="complex128")
         assert plan.binsize == 3 * 2 ** 24
-        # radix 5
+        # radix 5 and 7
         assert plan_create(5 * 2 ** 20, 3, dtype="complex64").binsize == 5 * 2 ** 17
+        assert plan_create(7 * 2 ** 20, 3, dtype="complex128").binsize == 7 * 2 ** 17
         with pytest.raises(errors.BinsizeNotPowerOfTwo):
-            plan_create(7 * 2 ** 10, 1, dtype="complex64", test_mode=True)
+            plan_create(9 * 2 ** 10, 1, dtype="complex64", test_mode=True)
 
     def test_binsize_minimum_holds_even_in_test_mode(self):
         assert plan_create(8, 1, workers=1, test_mode=True).binsize == 4

@@ -97,8 +97,9 @@ def test_split_sizes():
     n1, n2 = sharded.split_sizes(1 << 32, 4)
     assert n1 * n2 == 1 << 32 and n1 % 4 == 0 and n2 % 4 == 0
     assert sharded.split_sizes(5 << 20, 2) == (5 << 10, 1 << 10)
+    assert sharded.split_sizes(7 << 20, 2) == (7 << 10, 1 << 10)
     with pytest.raises(ValueError):
-        sharded.split_sizes(7 << 20, 2)
+        sharded.split_sizes(9 << 20, 2)
     with pytest.raises(ValueError):
         sharded.split_sizes(1 << 20, 3)
 
