@@ -452,6 +452,18 @@ constexpr int dif_pos(int L, int k) {
   }
   return pos;
 }
+// Same map with L a template parameter: every radix and stride is a
+// compile-time constant, so with k from an unrolled loop the position folds
+// to an immediate (register arrays stay in registers whatever the radix set).
+template <int L>
+__device__ __forceinline__ constexpr int dif_pos_t(int k) {
+  if constexpr (L <= 1) {
+    return 0;
+  } else {
+    constexpr int r = dif_radix_rt(L), q = L / r;
+    return (k % r) * q + dif_pos_t<q>(k / r);
+  }
+}
 
 template <typename R, int L, int B>
 __device__ __forceinline__ void dif_segment(typename CT<R>::V* v) {
@@ -609,7 +621,6 @@ struct Tile {
   }
 
   // register position of output t of an S-point in-place DFT
-  static constexpr int P(int S, int t) { return dif_pos(S, t); }
 
   static constexpr int prod_before(int i) {
     int p = 1;
@@ -682,8 +693,8 @@ struct Tile {
       const int k = u % NS;
 #pragma unroll
       for (int t = 0; t < S; ++t)
-        put(sm, fv * VEC, s, (u - k) * S + k + t * NS, &v[(q * VEC) * S + P(S, t)],
-            &v[(q * VEC + VEC - 1) * S + P(S, t)]);
+        put(sm, fv * VEC, s, (u - k) * S + k + t * NS, &v[(q * VEC) * S + dif_pos_t<S>(t)],
+            &v[(q * VEC + VEC - 1) * S + dif_pos_t<S>(t)]);
     }
   }
 
@@ -859,7 +870,7 @@ struct Tile {
         V y[VEC];
 #pragma unroll
         for (int c = 0; c < VEC; ++c) {
-          y[c] = v[(q * VEC + c) * SL + P(SL, t)];
+          y[c] = v[(q * VEC + c) * SL + dif_pos_t<SL>(t)];
           if constexpr (CS) y[c] = mk(y[c].x * sc, -y[c].y * sc);
         }
         if constexpr (MASK) {
@@ -889,7 +900,8 @@ struct Tile {
       coords<SL>(q, fv, u, s);
 #pragma unroll
       for (int t = 0; t < SL; ++t)
-        put(sm, fv * VEC, s, u + t * LL, &v[(q * VEC) * SL + P(SL, t)], &v[(q * VEC + VEC - 1) * SL + P(SL, t)]);
+        put(sm, fv * VEC, s, u + t * LL, &v[(q * VEC) * SL + dif_pos_t<SL>(t)],
+            &v[(q * VEC + VEC - 1) * SL + dif_pos_t<SL>(t)]);
     }
     tsync();
     constexpr int FAST = MODE == 1 ? D : RHO;

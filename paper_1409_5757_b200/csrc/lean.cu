@@ -63,7 +63,7 @@ struct LT {
 
 template <int S>
 __device__ __forceinline__ constexpr int P(int k) {
-  return dif_pos(S, k);
+  return dif_pos_t<S>(k);
 }
 
 // one element per lane: HBM stream (L1 bypass, L2 evict-first hint)
