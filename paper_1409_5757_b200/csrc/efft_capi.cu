@@ -703,7 +703,7 @@ int efft_plan_describe(efft_plan_t pl, char* buf, size_t len) {
     snprintf(line, sizeof line,
              "pass %d: R=%lld lean staged rho_a=%d rho_b=%d stages=[%dx%d | %dx16] grid=%d x %d smem=%d "
              "groups=%d tasks=%lld lag=%d slots=%d\n",
-             p, (long long)q.a.R, q.ra, q.rb, q.ra == 256 ? 16 : 12, 16, q.rb / 16, q.grid, q.nt, q.smem, q.a.ngroups,
+             p, (long long)q.a.R, q.ra, q.rb, q.ra / 16, 16, q.rb / 16, q.grid, q.nt, q.smem, q.a.ngroups,
              (long long)q.a.total,
              q.a.lag, q.a.nslots);
     s += line;

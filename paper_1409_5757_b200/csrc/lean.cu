@@ -1,6 +1,6 @@
 // lean.cu -- lean staged passes for the large DFTs: complex64 and complex128,
-// N = 2^k (2^26 <= N <= 2^32; complex64 from 2^24) and N = 3 * 2^k
-// (3 * 2^24 <= N <= 3 * 2^30).
+// N = 2^k (2^26 <= N <= 2^32; complex64 from 2^24) and N = M * 2^k, M in
+// {3, 5, 7} (about 2^24 .. 2^31 points).
 //
 // Same algorithm as the generic staged pass (efft_kernels.cuh: the four-step
 // form of the reference's scatter -> leaves -> merges, scatter.py:31-57,
@@ -22,8 +22,8 @@
 //     recurrences: no N-sized twiddle array is read.
 //
 // Index maps (N = R1 R2, R = RA RB per pass, j = ja + RB jb, k = kb + RA ka,
-// jb = s + A1 t, kb = kt + A0 ks (RA = A0 A1: 16 x 16, or 12 x 16 for the
-// factor 3), ja = p + 16 q, ka = kq + QB kp, QB = RB/16):
+// jb = s + A1 t, kb = kt + A0 ks (RA = A0 A1: 16 x 16, or 12 / 10 / 14 x 16
+// for the factor 3 / 5 / 7), ja = p + 16 q, ka = kq + QB kp, QB = RB/16):
 //   pass 1 (T1):  x[j2 + R2 j1] -> y[k1 + R1 j2] * W_N^(j2 k1); group = F j2
 //   pass 2 (T0):  y[k1 + R1 j2] -> X[k1 + R1 k2] in place;      group = F k1
 // Sub-stage A (per group: RB tiles of F lanes x RA jb, one ja each):
@@ -278,7 +278,7 @@ __global__ void __launch_bounds__(LT<R>::NT, MINB) lean_pass(const __grid_consta
   // W_(R/256)^i, i < R/256 and W_RA^i, i < RA (A inner twiddle): own tables
   // only when RA = 192; for RA = 256 both are strided views of W_256
   V* whi = RA == 256 ? w256 : wlo + 256;
-  V* wa = RA == 256 ? w256 : wlo + 256 + 192;
+  V* wa = RA == 256 ? w256 : wlo + 256 + RA;
   constexpr int HS = RA == 256 ? 256 / RB : 1;  // stride of whi
   __shared__ SchedShared shs;
   const int tid = threadIdx.x, lane = tid % F, r = tid / F;
@@ -291,7 +291,7 @@ __global__ void __launch_bounds__(LT<R>::NT, MINB) lean_pass(const __grid_consta
     w256[i] = to_v(wroot(i, 256), R());
     wlo[i] = to_v(wroot(i, a.R), R());
     if constexpr (RA != 256) {
-      if (i < 192) {  // R / 256 = 192 RB / 256 <= 192 and RA = 192 entries
+      if (i < RA) {  // R / 256 = RA RB / 256 <= RA and RA entries
         whi[i] = to_v(wroot(i, a.R / 256), R());
         wa[i] = to_v(wroot(i, RA), R());
       }
@@ -714,13 +714,13 @@ void build_tables(void* t4, int64_t n, int c128, cudaStream_t s) {
 
 template <typename R, int RA>
 static void* pick_ra(int rb, bool t1) {
-  if constexpr (RA == 192) {  // the factor 3 runs in the in-place pass only
+  if constexpr (RA != 256) {  // the odd factor runs in the in-place pass only
     if (t1) return nullptr;
     switch (rb) {
-      case 32: return (void*)lean_pass<R, 192, 32, false, 4>;
-      case 64: return (void*)lean_pass<R, 192, 64, false, 4>;
-      case 128: return (void*)lean_pass<R, 192, 128, false, 4>;
-      case 256: return (void*)lean_pass<R, 192, 256, false, 4>;
+      case 32: return (void*)lean_pass<R, RA, 32, false, 4>;
+      case 64: return (void*)lean_pass<R, RA, 64, false, 4>;
+      case 128: return (void*)lean_pass<R, RA, 128, false, 4>;
+      case 256: return (void*)lean_pass<R, RA, 256, false, 4>;
       default: return nullptr;
     }
   } else {
@@ -737,7 +737,12 @@ static void* pick_ra(int rb, bool t1) {
 // tiles have half the threads but 128 registers -- a fifth CTA would spill)
 template <typename R>
 static void* pick(int ra, int rb, bool t1) {
-  return ra == 192 ? pick_ra<R, 192>(rb, t1) : pick_ra<R, 256>(rb, t1);
+  switch (ra) {
+    case 192: return pick_ra<R, 192>(rb, t1);
+    case 160: return pick_ra<R, 160>(rb, t1);
+    case 224: return pick_ra<R, 224>(rb, t1);
+    default: return pick_ra<R, 256>(rb, t1);
+  }
 }
 static void* pick_pair(int rb, bool t1) {
   switch (rb) {
@@ -764,11 +769,12 @@ bool plan(int64_t n, int c128, int inverse, bool scale_inverse, bool check_finit
     m >>= 1;
     ++t;
   }
-  if (m != 1 && m != 3) return false;
+  if (m != 1 && m != 3 && m != 5 && m != 7) return false;
   // RA = 256, except RA = 192 in pass 2 (the in-place pass) when 3 | n;
   // log2(RB1 RB2) = t - 16 (or t - 14)
-  const int ra2 = m == 3 ? 192 : 256;
-  const int lbs = m == 3 ? t - 14 : t - 16;
+  // in-place pass: RA2 = 256, or 12 x 16 = 3 * 64, 10 x 16 = 5 * 32, 14 x 16 = 7 * 32
+  const int ra2 = m == 3 ? 192 : m == 5 ? 160 : m == 7 ? 224 : 256;
+  const int lbs = m == 1 ? t - 16 : m == 3 ? t - 14 : t - 13;
   const int lb1 = (lbs + 1) / 2, lb2 = lbs - lb1;
   // rho_b >= 32 (QB >= 2) in general; the paired complex64 kernel also runs
   // rho_b = 16 (QB = 1: the B stage is one 16-point DFT), down to N = 2^24
@@ -791,7 +797,7 @@ bool plan(int64_t n, int c128, int inverse, bool scale_inverse, bool check_finit
     q.nt = paired ? pair::NT : NT;
     // exchange (padded only in the transposing pass) + W_256 + W_R^(i<256) (+ two 192-entry tables)
     q.smem = paired ? (int)(((t1 ? pair::XB2 : 4096) + 512) * elem)
-                    : (int)(((t1 ? 256 * (F + 1) : 256 * F) + 512 + (q.ra == 256 ? 0 : 2 * 192)) * elem);
+                    : (int)(((t1 ? 256 * (F + 1) : 256 * F) + 512 + (q.ra == 256 ? 0 : 2 * q.ra)) * elem);
     Args& a = q.a;
     a = Args{};
     a.R = R;

@@ -1,9 +1,10 @@
 // lean.cuh -- host-side interface of the lean staged passes (lean.cu).
 //
 // The lean path runs the large power-of-two transforms (complex64 and
-// complex128, N = R1 * R2 with R = rho_a * rho_b, rho_a = 256 (or 192 in pass 1
-// for N = 3 * 2^k), rho_b in {32, 64, 128, 256} (also 16 for complex64):
-// 2^26 (2^24 for complex64) <= N <= 2^32 and 3 * 2^24 <= N <= 3 * 2^30) as two staged passes of one persistent kernel each:
+// complex128, N = R1 * R2 with R = rho_a * rho_b, rho_a = 256 (or 192 / 160 /
+// 224 in pass 2 for N = 3 / 5 / 7 * 2^k), rho_b in {32, 64, 128, 256} (also
+// 16 for complex64): 2^26 (2^24 for complex64) <= N <= 2^32 and the M * 2^k
+// families from about 2^24 to 2^30 points) as two staged passes of one persistent kernel each:
 //   pass 1: x[j2 + R2*j1] -> y[k1 + R1*j2] (DFT over j1, the four-step twiddle
 //           W_N^(j2*k1) fused into the store, the j2 <-> k1 transpose fused
 //           into sub-stage A's register exchange)

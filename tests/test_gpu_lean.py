@@ -84,6 +84,20 @@ def test_lean_radix3_family_vs_oracle(n, dtype):
 
 
 @pytest.mark.parametrize("dtype", ["complex64", "complex128"])
+@pytest.mark.parametrize("m,ra", [(5, 160), (7, 224)])
+def test_lean_radix5_radix7_families_vs_oracle(m, ra, dtype):
+    """N = 5 * 2^23, 7 * 2^23: the in-place pass runs rho_a = 10 x 16 / 14 x 16 tiles."""
+    n = m << 23
+    x = random_c(n, seed=m)
+    xd = torch.from_numpy(x.astype(NP[dtype])).cuda()
+    p, y = run(xd, dtype)
+    assert f"rho_a={ra}" in p.describe()
+    assert oracle.rel_l2(y.cpu().numpy(), oracle.transform(x)) <= tol(n, dtype)
+    _, z = run(y, dtype, direction=1)
+    assert oracle.rel_l2(z.cpu().numpy(), x) <= 2 * tol(n, dtype)
+
+
+@pytest.mark.parametrize("dtype", ["complex64", "complex128"])
 def test_lean_agrees_with_generic_staged_path(dtype, monkeypatch):
     n = 1 << 26
     x = torch.from_numpy(random_c(n, seed=7).astype(NP[dtype])).cuda()

@@ -29,7 +29,7 @@ c128 = len(sys.argv) > 2 and sys.argv[2] == "c128"
 tdt, ndt, esz = (torch.complex128, _native.EFFT_C128, 16) if c128 else (torch.complex64, _native.EFFT_C64, 8)
 for tok in logs:
     L = int(tok.split("x")[-1])
-    n = (3 if tok.startswith("3x") else 1) << L
+    n = (int(tok.split("x")[0]) if "x" in tok else 1) << L
     g = torch.Generator(device="cuda").manual_seed(L)
     x = torch.randn(n, dtype=tdt, device="cuda", generator=g)
     y = torch.empty_like(x)
