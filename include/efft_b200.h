@@ -61,7 +61,7 @@ extern "C" {
 typedef struct efft_plan_s *efft_plan_t;
 
 /* Plan one forward or inverse transform of n complex elements on `device`.
- * n must be M*2^t with M in {1,3}; allocates the staging ring and counters.
+ * n must be M*2^t with M in {1,3,5,7}; allocates the staging ring and counters.
  * The input buffer passed to efft_execute is never written; the output buffer
  * doubles as the pass-1 intermediate (out-of-place, two device arrays). */
 int efft_plan_create(efft_plan_t *plan, int64_t n, int dtype, int direction, int device,
