@@ -90,8 +90,8 @@ int efft_execute_host(efft_plan_t plan, const void *h_in, void *h_out, void *str
 /* `count` end-to-end transforms with host buffers (h_in[k] -> h_out[k]),
  * pipelined: transform k+1's host-to-device copy runs on an internal copy
  * stream while transform k computes and copies back on `stream`, so both PCIe
- * directions are busy at once (two device in/out pairs, allocated per call;
- * falls back to one-at-a-time efft_execute_host when they do not fit).
+ * directions are busy at once (two device in/out pairs from the per-device
+ * pool, kept for later calls; one at a time when the second pair does not fit).
  * Returns after the last copy-back has completed. */
 int efft_execute_host_batch(efft_plan_t plan, const void *const *h_in, void *const *h_out, int count,
                             void *stream);

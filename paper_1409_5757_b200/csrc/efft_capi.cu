@@ -77,6 +77,12 @@ struct HostPool {
   void* in = nullptr;
   void* out = nullptr;
   size_t bytes = 0;
+  // second pair, copy stream and events of efft_execute_host_batch (lazily created)
+  void* in2 = nullptr;
+  void* out2 = nullptr;
+  size_t bytes2 = 0;
+  cudaStream_t cs = nullptr;
+  cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
 };
 HostPool& host_pool(int device) {
   static HostPool pools[kMaxDevices];
@@ -822,64 +828,61 @@ int efft_execute_host_batch(efft_plan_t pl, const void* const* h_in, void* const
     if (!h_in[k] || !h_out[k]) return fail(EFFT_ERR_INVALID_ARG, "NULL host buffer %d", k);
   CUDA_TRY(cudaSetDevice(pl->device));
   const size_t bytes = (size_t)pl->n * pl->elem;
-  size_t free_b = 0, total_b = 0;
-  CUDA_TRY(cudaMemGetInfo(&free_b, &total_b));
-  if (count == 1 || free_b < 4 * bytes + (1ull << 30)) {  // no room for two in/out pairs: one at a time
-    for (int k = 0; k < count; ++k) {
-      int rc = efft_execute_host(pl, h_in[k], h_out[k], stream);
-      if (rc != EFFT_OK) return rc;
+  if (count == 1) return efft_execute_host(pl, h_in[0], h_out[0], stream);
+  HostPool& hp = host_pool(pl->device);
+  std::lock_guard<std::mutex> lock(hp.mu);
+  // two device in/out pairs from the per-device pool (grown on demand; when
+  // they do not fit, one transform at a time through the first pair)
+  auto grow = [&](void*& i, void*& o, size_t& have) -> bool {
+    if (have >= bytes) return true;
+    if (i) cudaFree(i);
+    if (o) cudaFree(o);
+    i = o = nullptr;
+    have = 0;
+    if (cudaMalloc(&i, bytes) != cudaSuccess || cudaMalloc(&o, bytes) != cudaSuccess) {
+      cudaGetLastError();
+      if (i) cudaFree(i);
+      i = nullptr;
+      return false;
     }
+    have = bytes;
+    return true;
+  };
+  if (!grow(hp.in, hp.out, hp.bytes)) return fail(EFFT_ERR_ALLOC, "device buffers for host execution (%zu bytes each)", bytes);
+  cudaStream_t s = (cudaStream_t)stream;
+  if (!grow(hp.in2, hp.out2, hp.bytes2)) {  // sequential fallback
+    for (int k = 0; k < count; ++k) {
+      CUDA_TRY(cudaMemcpyAsync(hp.in, h_in[k], bytes, cudaMemcpyHostToDevice, s));
+      int rc = efft_execute(pl, hp.in, hp.out, stream);
+      if (rc != EFFT_OK) return rc;
+      CUDA_TRY(cudaMemcpyAsync(h_out[k], hp.out, bytes, cudaMemcpyDeviceToHost, s));
+    }
+    CUDA_TRY(cudaStreamSynchronize(s));
     return EFFT_OK;
   }
-  // Two device in/out pairs; transform k+1's H2D (copy stream) overlaps
-  // transform k's passes and D2H (the caller's stream): the two PCIe
-  // directions run concurrently.
-  void* din[2] = {nullptr, nullptr};
-  void* dout[2] = {nullptr, nullptr};
-  cudaStream_t s = (cudaStream_t)stream, cs = nullptr;
-  cudaEvent_t in_ready[2] = {nullptr, nullptr}, buf_free[2] = {nullptr, nullptr};
-  int rc = EFFT_OK;
-  auto cleanup = [&]() {
-    for (int b = 0; b < 2; ++b) {
-      if (din[b]) cudaFree(din[b]);
-      if (dout[b]) cudaFree(dout[b]);
-      if (in_ready[b]) cudaEventDestroy(in_ready[b]);
-      if (buf_free[b]) cudaEventDestroy(buf_free[b]);
-    }
-    if (cs) cudaStreamDestroy(cs);
-  };
-  for (int b = 0; b < 2 && rc == EFFT_OK; ++b) {
-    if (cudaMalloc(&din[b], bytes) != cudaSuccess || cudaMalloc(&dout[b], bytes) != cudaSuccess ||
-        cudaEventCreateWithFlags(&in_ready[b], cudaEventDisableTiming) != cudaSuccess ||
-        cudaEventCreateWithFlags(&buf_free[b], cudaEventDisableTiming) != cudaSuccess) {
-      cudaGetLastError();
-      rc = fail(EFFT_ERR_ALLOC, "double-buffered host execution (%zu bytes x 4)", bytes);
-    }
-  }
-  if (rc == EFFT_OK && cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking) != cudaSuccess)
-    rc = fail(EFFT_ERR_CUDA, "copy stream");
-  if (rc == EFFT_OK && cudaEventRecord(buf_free[0], s) != cudaSuccess) rc = fail(EFFT_ERR_CUDA, "event");
-  if (rc == EFFT_OK && cudaEventRecord(buf_free[1], s) != cudaSuccess) rc = fail(EFFT_ERR_CUDA, "event");
-  for (int k = 0; k < count && rc == EFFT_OK; ++k) {
+  if (!hp.cs) CUDA_TRY(cudaStreamCreateWithFlags(&hp.cs, cudaStreamNonBlocking));
+  for (auto& e : hp.ev)
+    if (!e) CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  // Transform k+1's H2D (copy stream) overlaps transform k's passes and D2H
+  // (the caller's stream): the two PCIe directions run concurrently.
+  void* din[2] = {hp.in, hp.in2};
+  void* dout[2] = {hp.out, hp.out2};
+  cudaEvent_t in_ready[2] = {hp.ev[0], hp.ev[1]}, buf_free[2] = {hp.ev[2], hp.ev[3]};
+  CUDA_TRY(cudaEventRecord(buf_free[0], s));
+  CUDA_TRY(cudaEventRecord(buf_free[1], s));
+  for (int k = 0; k < count; ++k) {
     const int b = k & 1;
-    if (cudaStreamWaitEvent(cs, buf_free[b], 0) != cudaSuccess ||
-        cudaMemcpyAsync(din[b], h_in[k], bytes, cudaMemcpyHostToDevice, cs) != cudaSuccess ||
-        cudaEventRecord(in_ready[b], cs) != cudaSuccess || cudaStreamWaitEvent(s, in_ready[b], 0) != cudaSuccess) {
-      rc = fail(EFFT_ERR_CUDA, "batch copy-in %d: %s", k, cudaGetErrorString(cudaGetLastError()));
-      break;
-    }
-    rc = efft_execute(pl, din[b], dout[b], stream);
-    if (rc != EFFT_OK) break;
-    if (cudaMemcpyAsync(h_out[k], dout[b], bytes, cudaMemcpyDeviceToHost, s) != cudaSuccess ||
-        cudaEventRecord(buf_free[b], s) != cudaSuccess) {
-      rc = fail(EFFT_ERR_CUDA, "batch copy-out %d: %s", k, cudaGetErrorString(cudaGetLastError()));
-      break;
-    }
+    CUDA_TRY(cudaStreamWaitEvent(hp.cs, buf_free[b], 0));
+    CUDA_TRY(cudaMemcpyAsync(din[b], h_in[k], bytes, cudaMemcpyHostToDevice, hp.cs));
+    CUDA_TRY(cudaEventRecord(in_ready[b], hp.cs));
+    CUDA_TRY(cudaStreamWaitEvent(s, in_ready[b], 0));
+    int rc = efft_execute(pl, din[b], dout[b], stream);
+    if (rc != EFFT_OK) return rc;
+    CUDA_TRY(cudaMemcpyAsync(h_out[k], dout[b], bytes, cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaEventRecord(buf_free[b], s));
   }
-  if (cudaStreamSynchronize(s) != cudaSuccess && rc == EFFT_OK) rc = fail(EFFT_ERR_CUDA, "batch sync");
-  if (cs && cudaStreamSynchronize(cs) != cudaSuccess && rc == EFFT_OK) rc = fail(EFFT_ERR_CUDA, "batch sync");
-  cleanup();
-  return rc;
+  CUDA_TRY(cudaStreamSynchronize(s));
+  return EFFT_OK;
 }
 
 int efft_release_host_buffers(int device) {
@@ -889,8 +892,10 @@ int efft_release_host_buffers(int device) {
   CUDA_TRY(cudaSetDevice(device));
   if (hp.in) cudaFree(hp.in);
   if (hp.out) cudaFree(hp.out);
-  hp.in = hp.out = nullptr;
-  hp.bytes = 0;
+  if (hp.in2) cudaFree(hp.in2);
+  if (hp.out2) cudaFree(hp.out2);
+  hp.in = hp.out = hp.in2 = hp.out2 = nullptr;
+  hp.bytes = hp.bytes2 = 0;
   return EFFT_OK;
 }
 
