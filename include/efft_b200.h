@@ -96,6 +96,21 @@ int efft_execute_host(efft_plan_t plan, const void *h_in, void *h_out, void *str
 int efft_execute_host_batch(efft_plan_t plan, const void *const *h_in, void *const *h_out, int count,
                             void *stream);
 
+/* Out-of-core transform of a HOST array larger than HBM (the
+ * paper's "enormous" N, reference bench.py:115-126 reads binary32 arrays from
+ * disk): N = N1 N2 four-step over host memory with at most about
+ * `device_bytes` of device buffers (two streams x two buffers), strided DMA
+ * straight from / to h_in and h_out (page-locked for the call), block k+1's
+ * copies overlapping block k's.  h_out doubles as the intermediate; h_in is
+ * not modified; they must not overlap.  N = M 2^t, M in {1,3,5,7},
+ * N1, N2 <= 2^17.  Synchronous.  Inverse scaled by 1/N with
+ * EFFT_FLAG_SCALE_INVERSE. */
+int efft_execute_outofcore(int64_t n, int dtype, int direction, int device, uint32_t flags, const void *h_in,
+                           void *h_out, size_t device_bytes);
+/* The split and block sizes efft_execute_outofcore uses: blocks[0..3] =
+ * N1, N2, columns per step-1 block, rows per step-2 block.  Host only. */
+int efft_outofcore_blocks(int64_t n, int dtype, size_t device_bytes, int64_t *blocks);
+
 /* Frees the per-device pool of efft_execute_host (it is re-created on demand). */
 int efft_release_host_buffers(int device);
 

@@ -44,6 +44,8 @@ EXPORTED = (
     "efft_execute_host",
     "efft_release_host_buffers",
     "efft_execute_host_batch",
+    "efft_execute_outofcore",
+    "efft_outofcore_blocks",
     "efft_nonfinite_seen",
     "efft_plan_destroy",
     "efft_plan_enable_timing",
@@ -80,6 +82,8 @@ def load():
     lib.efft_execute_host.argtypes = [vp, vp, vp, vp]
     lib.efft_release_host_buffers.argtypes = [i32]
     lib.efft_execute_host_batch.argtypes = [vp, ctypes.POINTER(vp), ctypes.POINTER(vp), i32, vp]
+    lib.efft_execute_outofcore.argtypes = [i64, i32, i32, i32, u32, vp, vp, ctypes.c_size_t]
+    lib.efft_outofcore_blocks.argtypes = [i64, i32, ctypes.c_size_t, ctypes.POINTER(i64)]
     lib.efft_nonfinite_seen.argtypes = [vp, ctypes.POINTER(i32), vp]
     lib.efft_plan_destroy.argtypes = [vp]
     lib.efft_plan_enable_timing.argtypes = [vp, i32]
@@ -107,6 +111,19 @@ def check(rc: int, what: str = "") -> None:
 
 def release_host_buffers(device: int = 0) -> None:
     check(load().efft_release_host_buffers(device), "efft_release_host_buffers")
+
+
+def outofcore_blocks(n: int, dtype: int, device_bytes: int):
+    """(N1, N2, columns per step-1 block, rows per step-2 block) -- host only."""
+    b = (ctypes.c_int64 * 4)()
+    check(load().efft_outofcore_blocks(n, dtype, device_bytes, b), "efft_outofcore_blocks")
+    return tuple(int(v) for v in b)
+
+
+def execute_outofcore(n: int, dtype: int, direction: int, device: int, flags: int, h_in: int, h_out: int,
+                      device_bytes: int) -> None:
+    check(load().efft_execute_outofcore(n, dtype, direction, device, flags, h_in, h_out, device_bytes),
+          "efft_execute_outofcore")
 
 
 def permute_swap01(d_in: int, d_out: int, n0: int, n1: int, n2: int, elem: int, stream: int) -> None:

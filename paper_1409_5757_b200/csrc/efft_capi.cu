@@ -885,6 +885,138 @@ int efft_execute_host_batch(efft_plan_t pl, const void* const* h_in, void* const
   return EFFT_OK;
 }
 
+// ---- out-of-core transform ----------------------------
+// N = N1 N2 (N1 takes the odd factor), x viewed as (N1 x N2) row-major.
+//   step 1  per block of C columns n2: strided H2D DMA of x[:, c0:c0+C], a
+//           column plan of length N1, a device transpose -> rows c0.. of
+//           Yt[n2][k1] (= h_out, contiguous D2H)
+//   step 2  per block of Rr columns k1 of Yt: strided H2D DMA, a column plan
+//           of length N2 with the four-step twiddle W_N^(n2 k1), strided D2H
+//           into the SAME columns of h_out viewed as X[k2][k1]
+// Step 2 reads each block of h_out exactly where it writes it back, so the
+// host intermediate costs no memory.  Blocks alternate between two streams and
+// two device buffer sets: one block's H2D overlaps the other's D2H and plan.
+// The host buffers are page-locked for the call (cudaHostRegister) so every
+// copy is a DMA straight from / to the caller's arrays.
+namespace {
+int64_t ooc_fit(int64_t length, int64_t dim, int64_t per, int64_t f) {
+  int64_t b = std::max(f, std::min(dim, per / length));
+  b -= b % f;
+  b = std::max(f, b);
+  while (b >= f && dim % b) b -= f;
+  return (b >= f && dim % b == 0) ? b : 0;
+}
+}  // namespace
+
+int efft_outofcore_blocks(int64_t n, int dtype, size_t device_bytes, int64_t* blocks) {
+  if (!blocks) return fail(EFFT_ERR_INVALID_ARG, "blocks is NULL");
+  if (dtype != EFFT_C64 && dtype != EFFT_C128) return fail(EFFT_ERR_INVALID_ARG, "dtype %d", dtype);
+  int M, t;
+  if (n < 4 || !factor(n, &M, &t)) return fail(EFFT_ERR_UNSUPPORTED_SIZE, "n=%lld is not M*2^t with M in {1,3,5,7}", (long long)n);
+  const int t1 = t / 2;
+  const int64_t n1 = (int64_t)M << t1, n2 = (int64_t)1 << (t - t1);
+  if (n1 > (1 << 17) || n2 > (1 << 17))
+    return fail(EFFT_ERR_UNSUPPORTED_SIZE, "n=%lld exceeds the out-of-core range (N1, N2 <= 2^17)", (long long)n);
+  const int64_t e = dtype == EFFT_C64 ? 8 : 16, f = dtype == EFFT_C64 ? 16 : 8;
+  const int64_t per = std::max<int64_t>(1, (int64_t)(device_bytes / (4 * e)));  // 2 streams x 2 buffers
+  const int64_t cb = ooc_fit(n1, n2, per, f), rb = ooc_fit(n2, n1, per, f);
+  if (!cb || !rb) return fail(EFFT_ERR_UNSUPPORTED_SIZE, "no block of n=%lld fits %zu bytes", (long long)n, device_bytes);
+  blocks[0] = n1;
+  blocks[1] = n2;
+  blocks[2] = cb;
+  blocks[3] = rb;
+  return EFFT_OK;
+}
+
+int efft_execute_outofcore(int64_t n, int dtype, int direction, int device, uint32_t flags, const void* h_in,
+                           void* h_out, size_t device_bytes) {
+  if (!h_in || !h_out) return fail(EFFT_ERR_INVALID_ARG, "NULL host buffer");
+  if (direction != EFFT_FORWARD && direction != EFFT_INVERSE)
+    return fail(EFFT_ERR_INVALID_ARG, "direction must be -1 or +1, got %d", direction);
+  int64_t bl[4];
+  int rc = efft_outofcore_blocks(n, dtype, device_bytes, bl);
+  if (rc != EFFT_OK) return rc;
+  const int64_t n1 = bl[0], n2 = bl[1], cb = bl[2], rb = bl[3];
+  const size_t e = dtype == EFFT_C64 ? 8 : 16, bytes = (size_t)n * e;
+  const char* hi = (const char*)h_in;
+  char* ho = (char*)h_out;
+  if (hi < ho + bytes && ho < hi + bytes) return fail(EFFT_ERR_INVALID_ARG, "input and output overlap");
+  int ndev = 0;
+  CUDA_TRY(cudaGetDeviceCount(&ndev));
+  if (device < 0 || device >= ndev) return fail(EFFT_ERR_INVALID_ARG, "device %d of %d", device, ndev);
+  CUDA_TRY(cudaSetDevice(device));
+  struct Res {  // released on every exit path
+    efft_plan_t p1[2] = {nullptr, nullptr}, p2[2] = {nullptr, nullptr};
+    void* a[2] = {nullptr, nullptr};
+    void* b[2] = {nullptr, nullptr};
+    cudaStream_t s[2] = {nullptr, nullptr};
+    void* reg[2] = {nullptr, nullptr};
+    ~Res() {
+      for (int i = 0; i < 2; ++i) {
+        if (s[i]) cudaStreamSynchronize(s[i]);
+      }
+      for (int i = 0; i < 2; ++i) {
+        if (p1[i]) efft_plan_destroy(p1[i]);
+        if (p2[i]) efft_plan_destroy(p2[i]);
+        if (a[i]) cudaFree(a[i]);
+        if (b[i]) cudaFree(b[i]);
+        if (s[i]) cudaStreamDestroy(s[i]);
+        if (reg[i]) cudaHostUnregister(reg[i]);
+      }
+    }
+  } r;
+  for (int i = 0; i < 2; ++i) {
+    void* ptr = i == 0 ? (void*)hi : (void*)ho;
+    cudaPointerAttributes at{};
+    if (cudaPointerGetAttributes(&at, ptr) == cudaSuccess && at.type == cudaMemoryTypeHost) continue;  // caller-pinned
+    cudaGetLastError();
+    cudaError_t er = cudaHostRegister(ptr, bytes, cudaHostRegisterDefault);
+    if (er == cudaSuccess) r.reg[i] = ptr;
+    else if (er == cudaErrorHostMemoryAlreadyRegistered) cudaGetLastError();  // caller-pinned: keep as is
+    else {
+      cudaGetLastError();
+      return fail(EFFT_ERR_CUDA, "cudaHostRegister of %zu bytes: %s", bytes, cudaGetErrorString(er));
+    }
+  }
+  const size_t buf = (size_t)std::max(n1 * cb, n2 * rb) * e;
+  const uint32_t pf = flags & (EFFT_FLAG_SCALE_INVERSE | EFFT_FLAG_CHECK_FINITE);
+  for (int i = 0; i < 2; ++i) {
+    if (cudaMalloc(&r.a[i], buf) != cudaSuccess || cudaMalloc(&r.b[i], buf) != cudaSuccess) {
+      cudaGetLastError();
+      return fail(EFFT_ERR_ALLOC, "out-of-core device buffers (4 x %zu bytes)", buf);
+    }
+    CUDA_TRY(cudaStreamCreateWithFlags(&r.s[i], cudaStreamNonBlocking));
+    rc = efft_plan_create_columns(&r.p1[i], n1, cb, dtype, direction, device, 0, 0, pf);
+    if (rc != EFFT_OK) return rc;
+    rc = efft_plan_create_columns(&r.p2[i], n2, rb, dtype, direction, device, n, 0, pf);
+    if (rc != EFFT_OK) return rc;
+  }
+  // step 1
+  for (int64_t c0 = 0, k = 0; c0 < n2; c0 += cb, ++k) {
+    const int i = (int)(k & 1);
+    CUDA_TRY(cudaMemcpy2DAsync(r.a[i], cb * e, hi + c0 * e, n2 * e, cb * e, n1, cudaMemcpyHostToDevice, r.s[i]));
+    rc = efft_execute(r.p1[i], r.a[i], r.a[i], r.s[i]);
+    if (rc != EFFT_OK) return rc;
+    rc = efft_permute_swap01(r.a[i], r.b[i], n1, cb, 1, (int)e, r.s[i]);  // [k1][c] -> [c][k1]
+    if (rc != EFFT_OK) return rc;
+    CUDA_TRY(cudaMemcpyAsync(ho + c0 * n1 * e, r.b[i], cb * n1 * e, cudaMemcpyDeviceToHost, r.s[i]));
+  }
+  for (int i = 0; i < 2; ++i) CUDA_TRY(cudaStreamSynchronize(r.s[i]));
+  // step 2 (the twiddle offset of a column plan is the first k1 of its block)
+  for (int64_t r0 = 0, k = 0; r0 < n1; r0 += rb, ++k) {
+    const int i = (int)(k & 1);
+    efft_plan_s* p2 = r.p2[i];
+    p2->col_tw_offset = r0;
+    p2->pass[0].args.a.A0 = r0;
+    CUDA_TRY(cudaMemcpy2DAsync(r.a[i], rb * e, ho + r0 * e, n1 * e, rb * e, n2, cudaMemcpyHostToDevice, r.s[i]));
+    rc = efft_execute(p2, r.a[i], r.a[i], r.s[i]);
+    if (rc != EFFT_OK) return rc;
+    CUDA_TRY(cudaMemcpy2DAsync(ho + r0 * e, n1 * e, r.a[i], rb * e, rb * e, n2, cudaMemcpyDeviceToHost, r.s[i]));
+  }
+  for (int i = 0; i < 2; ++i) CUDA_TRY(cudaStreamSynchronize(r.s[i]));
+  return EFFT_OK;
+}
+
 int efft_release_host_buffers(int device) {
   if (device < 0 || device >= kMaxDevices) return fail(EFFT_ERR_INVALID_ARG, "device %d", device);
   HostPool& hp = host_pool(device);

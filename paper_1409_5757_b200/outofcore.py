@@ -12,10 +12,13 @@ with bounded device buffers.  With N = N1 N2, x viewed as (N1 x N2) row-major
           (contiguous rows H2D, device transpose, a column plan with the
           four-step twiddle on its input, D2H into X viewed as (N2 x N1))
 
-Both steps use the library's column plans (efft_plan_create_columns) and the
-permutation kernel (efft_permute_swap01); the host side only reshuffles
-blocks.  Inverse = direction +1 with 1/N1 and 1/N2 scaling in the two column
-plans (1/N in total).  Sizes N = M 2^t, M in {1, 3, 5, 7}, N1, N2 <= 2^17.
+The streaming runs natively (efft_execute_outofcore in efft_capi.cu): the
+caller's arrays are page-locked for the call, every block moves by strided
+DMA (no host-side reshuffle), step 1 writes Y transposed (Yt[n2][k1]) into the
+output array and step 2 transforms it in place block by block, with two
+streams and two device buffer sets so one block's copies overlap the other's.
+Inverse = direction +1 with 1/N1 and 1/N2 scaling in the two column plans
+(1/N in total).  Sizes N = M 2^t, M in {1, 3, 5, 7}, N1, N2 <= 2^17.
 """
 
 import math
@@ -46,14 +49,15 @@ def split(n: int):
 
 
 def plan_blocks(n: int, dtype: str, device_bytes: int):
-    """Columns per step-1 block and rows per step-2 block for a device budget.
+    """Columns per step-1 block and rows per step-2 block for a device budget
+    (mirror of efft_outofcore_blocks).
 
-    Each step holds two device buffers of its block (in/out of the column plan
-    or of the transpose).  Blocks are multiples of the 128-byte line width and
-    divide the array dimension."""
+    Two streams each hold two device buffers of a block (in/out of the column
+    plan or of the transpose).  Blocks are multiples of the 128-byte line width
+    and divide the array dimension."""
     n1, n2 = split(n)
     e, f = ELEM[dtype], LANES[dtype]
-    per = max(1, device_bytes // (2 * e))  # elements per buffer
+    per = max(1, device_bytes // (4 * e))  # elements per buffer
 
     def fit(length, dim):
         b = max(f, min(dim, per // length))
@@ -72,50 +76,18 @@ def transform(x: np.ndarray, direction: int = -1, device: int = 0, device_bytes:
               out: np.ndarray = None) -> np.ndarray:
     """DFT of host array `x` (complex64 / complex128, natural order) with at most
     about `device_bytes` of device memory for the data blocks."""
-    import torch
-
-    dtype = "complex64" if x.dtype == np.complex64 else "complex128"
     if x.dtype not in (np.complex64, np.complex128) or x.ndim != 1:
         raise ValueError("x must be a 1D complex64 or complex128 array")
+    dtype = "complex64" if x.dtype == np.complex64 else "complex128"
     n = x.shape[0]
-    n1, n2, cblk, rblk = plan_blocks(n, dtype, device_bytes)
+    plan_blocks(n, dtype, device_bytes)  # validates (same rule as the library)
+    x = np.ascontiguousarray(x)
+    res = out if out is not None else np.empty(n, dtype=x.dtype)
+    if res.dtype != x.dtype or res.shape != (n,) or not res.flags.c_contiguous:
+        raise ValueError("out must be a contiguous array like x")
     ndt = _native.EFFT_C64 if dtype == "complex64" else _native.EFFT_C128
     flags = _native.EFFT_FLAG_SCALE_INVERSE if direction == 1 else 0
-    tdt = torch.complex64 if dtype == "complex64" else torch.complex128
-    dev = torch.device("cuda", device)
-    y = np.empty((n1, n2), dtype=x.dtype)  # host intermediate Y[k1][n2]
-    res = out if out is not None else np.empty(n, dtype=x.dtype)
-    x2 = x.reshape(n1, n2)
-    xr = res.reshape(n2, n1)  # X[k1 + N1 k2] viewed as [k2][k1]
-    with torch.cuda.device(device):
-        s = torch.cuda.current_stream().cuda_stream
-        a = torch.empty(max(n1 * cblk, n2 * rblk), dtype=tdt, device=dev)
-        b = torch.empty_like(a)
-        pin = torch.empty(a.numel(), dtype=tdt, pin_memory=True)
-        pin_np = pin.numpy()
-        # step 1: column DFTs of length N1 over blocks of C columns
-        p1 = _native.NativePlan(n1, ndt, direction, device, flags, columns=(cblk, 0, 0))
-        for c0 in range(0, n2, cblk):
-            blk = pin_np[: n1 * cblk].reshape(n1, cblk)
-            np.copyto(blk, x2[:, c0:c0 + cblk])
-            a[: n1 * cblk].copy_(pin[: n1 * cblk], non_blocking=True)
-            p1.execute(a.data_ptr(), a.data_ptr(), s)
-            pin[: n1 * cblk].copy_(a[: n1 * cblk], non_blocking=True)
-            torch.cuda.current_stream().synchronize()
-            y[:, c0:c0 + cblk] = blk
-        p1.close()
-        # step 2: twiddle W_N^(n2 k1) + DFTs of length N2 over blocks of Rr rows k1
-        for r0 in range(0, n1, rblk):
-            p2 = _native.NativePlan(n2, ndt, direction, device, flags, columns=(rblk, n, r0))
-            m = n2 * rblk
-            np.copyto(pin_np[:m].reshape(rblk, n2), y[r0:r0 + rblk])
-            a[:m].copy_(pin[:m], non_blocking=True)
-            _native.permute_swap01(a.data_ptr(), b.data_ptr(), rblk, n2, 1, ELEM[dtype], s)  # -> [n2][r]
-            p2.execute(b.data_ptr(), b.data_ptr(), s)  # -> [k2][r]
-            pin[:m].copy_(b[:m], non_blocking=True)
-            torch.cuda.current_stream().synchronize()
-            xr[:, r0:r0 + rblk] = pin_np[:m].reshape(n2, rblk)
-            p2.close()
+    _native.execute_outofcore(n, ndt, direction, device, flags, x.ctypes.data, res.ctypes.data, device_bytes)
     return res
 
 

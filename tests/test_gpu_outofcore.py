@@ -50,3 +50,21 @@ def test_out_of_core_matches_in_hbm_transform_at_2p28():
     y = outofcore.transform(x, device_bytes=n * 8 // 16)
     err = float(np.linalg.norm(y.astype(np.complex128) - ref) / np.linalg.norm(ref.astype(np.complex128)))
     assert err <= 2 * tol(n, np.complex64)
+
+
+def test_out_of_core_caller_pinned_buffers_and_out_argument():
+    """Buffers the caller already page-locked (cudaHostRegister reports them as
+    registered) are used as they are and stay pinned; `out` is written in place."""
+    n = 3 << 20
+    x = torch.from_numpy(random_c(n, seed=5).astype(np.complex64)).pin_memory()
+    o = torch.empty(n, dtype=torch.complex64).pin_memory()
+    y = outofcore.transform(x.numpy(), device_bytes=1 << 20, out=o.numpy())
+    assert y.ctypes.data == o.data_ptr()
+    assert oracle.rel_l2(y, oracle.transform(x.numpy().astype(np.complex128))) <= tol(n, np.complex64)
+    assert x.is_pinned() and o.is_pinned()
+
+
+def test_out_of_core_rejects_overlap():
+    x = random_c(1 << 20, seed=1).astype(np.complex64)
+    with pytest.raises(ValueError, match="overlap"):  # EFFT_ERR_INVALID_ARG
+        outofcore.transform(x, out=x)

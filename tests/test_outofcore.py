@@ -24,5 +24,22 @@ def test_blocks_fit_budget_and_tile_the_array(n, dtype, budget):
     e, f = outofcore.ELEM[dtype], outofcore.LANES[dtype]
     assert n1 * n2 == n
     assert n2 % cb == 0 and n1 % rb == 0 and cb % f == 0 and rb % f == 0
-    assert 2 * n1 * cb * e <= max(budget, 2 * n1 * f * e)
-    assert 2 * n2 * rb * e <= max(budget, 2 * n2 * f * e)
+    assert 4 * n1 * cb * e <= max(budget, 4 * n1 * f * e)
+    assert 4 * n2 * rb * e <= max(budget, 4 * n2 * f * e)
+
+
+@pytest.mark.parametrize("n", [1 << 8, 1 << 20, 3 << 20, 5 << 21, 7 << 19, 1 << 30, 1 << 34])
+@pytest.mark.parametrize("dtype", ["complex64", "complex128"])
+@pytest.mark.parametrize("budget", [1 << 16, 1 << 22, 1 << 30])
+def test_python_mirror_matches_library_block_rule(n, dtype, budget):
+    """outofcore.plan_blocks restates efft_outofcore_blocks (host-only query, no GPU)."""
+    from paper_1409_5757_b200 import _native
+
+    ndt = _native.EFFT_C64 if dtype == "complex64" else _native.EFFT_C128
+    try:
+        want = outofcore.plan_blocks(n, dtype, budget)
+    except BinsizeNotPowerOfTwo:
+        with pytest.raises(BinsizeNotPowerOfTwo):
+            _native.outofcore_blocks(n, ndt, budget)
+        return
+    assert _native.outofcore_blocks(n, ndt, budget) == want
