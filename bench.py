@@ -21,6 +21,10 @@ Prints ONE JSON line (rank 0).  Keys beyond the base contract:
                 passes -> D2H -> host out, with transform k+1's H2D overlapping
                 transform k's passes and D2H (the two PCIe directions at once);
                 forward+inverse configs chain efft_execute_host calls
+  fp64          complex128 configs: the fp64 arithmetic rate (nominal 5NlogN and
+                executed DADD+DMUL+2*DFMA from the committed ncu counts) against
+                the measured DFMA peak (tools/dfma_peak.cu) -- 20 % of it: the
+                passes are HBM bound, not fp64 bound
 --impl reference times that CPU restatement (the reference itself is Python and
 cannot travel to the GPU box) and prints the same line shape.
 Multi-GPU (torchrun): ONE transform of the config's N, six-step sharded over the
@@ -376,6 +380,24 @@ def run_ours(args):
     except (OSError, ValueError, KeyError, IndexError):
         traffic = None
     whole_gbs = per_step * fwd.launches() * alg_bytes / (ms_per_step * 1e-3) / 1e9
+    desc = fwd.describe()
+    kname = (("lean_pair" if dtype == "complex64" else "lean_pass") if "lean" in desc
+             else "generic staged/direct pass")
+    fp64 = None  # complex128: fp64 arithmetic rate vs the measured DFMA peak
+    if dtype == "complex128":
+        try:
+            with open(os.path.join(ROOT, "profiles", "fp64.json")) as fh:
+                f64 = json.load(fh)
+            ratio = f64.get(args.config, {}).get("executed_over_nominal")
+            dpk = f64["dfma_peak"]["dfma_tflops"]
+            nominal = value / 1e3
+            fp64 = {"nominal_tflops": round(nominal, 3), "dfma_peak_tflops": dpk,
+                    "executed_over_nominal": ratio,
+                    "executed_tflops": round(nominal * ratio, 3) if ratio else None,
+                    "frac": round(nominal * (ratio or 1.0) / dpk, 4),
+                    "source": "profiles/fp64.json (ncu DADD+DMUL+2*DFMA counts; tools/dfma_peak.cu)"}
+        except (OSError, ValueError, KeyError):
+            fp64 = None
 
     # e2e through the C-ABI host-buffer entry (rank-local), fewer steps: PCIe bound
     e2e = None
@@ -429,13 +451,14 @@ def run_ours(args):
                        "n": n, "input": cfg["kind"], "parallelism": f"replicas x{world}",
                        "l2": "flushed between steps (512 MiB write)" if flush is not None
                              else f"inputs ({n * ELEM[dtype] >> 20} MiB) larger than L2",
-                       "plan": fwd.describe().strip().splitlines()},
+                       "plan": desc.strip().splitlines()},
             "hbm_gbs_whole_step": round(whole_gbs, 1),
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
                          "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": traffic,
-                         "kernel": f"pass {dom} of {len(avg)} (lean_pass kernel), {avg[dom]:.4f} ms avg",
+                         "kernel": f"pass {dom} of {len(avg)} ({kname} kernel), {avg[dom]:.4f} ms avg",
                          "pass_ms": [round(a, 4) for a in avg], "peak_source": peak_src,
                          "alg_bytes_per_launch": alg_bytes},
+            "fp64": fp64,
             "gpu_launches": launches * args.steps,
             "clocks": clocks.summary(),
             "e2e": e2e,
