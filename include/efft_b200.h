@@ -102,7 +102,8 @@ int efft_execute_host_batch(efft_plan_t plan, const void *const *h_in, void *con
  * `device_bytes` of device buffers (two streams x two buffers), strided DMA
  * straight from / to h_in and h_out (page-locked for the call), block k+1's
  * copies overlapping block k's.  h_out doubles as the intermediate; h_in is
- * not modified; they must not overlap.  N = M 2^t, M in {1,3,5,7},
+ * not modified (read-only memory, e.g. a read-only file mapping, is read
+ * through pinned staging buffers); they must not overlap.  N = M 2^t, M in {1,3,5,7},
  * N1, N2 <= 2^17.  Synchronous.  Inverse scaled by 1/N with
  * EFFT_FLAG_SCALE_INVERSE. */
 int efft_execute_outofcore(int64_t n, int dtype, int direction, int device, uint32_t flags, const void *h_in,

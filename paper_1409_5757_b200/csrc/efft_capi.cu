@@ -951,6 +951,8 @@ int efft_execute_outofcore(int64_t n, int dtype, int direction, int device, uint
     void* b[2] = {nullptr, nullptr};
     cudaStream_t s[2] = {nullptr, nullptr};
     void* reg[2] = {nullptr, nullptr};
+    void* stage[2] = {nullptr, nullptr};  // pinned step-1 staging when h_in cannot be page-locked
+    cudaEvent_t ev[2] = {nullptr, nullptr};
     ~Res() {
       for (int i = 0; i < 2; ++i) {
         if (s[i]) cudaStreamSynchronize(s[i]);
@@ -962,15 +964,25 @@ int efft_execute_outofcore(int64_t n, int dtype, int direction, int device, uint
         if (b[i]) cudaFree(b[i]);
         if (s[i]) cudaStreamDestroy(s[i]);
         if (reg[i]) cudaHostUnregister(reg[i]);
+        if (stage[i]) cudaFreeHost(stage[i]);
+        if (ev[i]) cudaEventDestroy(ev[i]);
       }
     }
   } r;
+  bool staged_in = false;
   for (int i = 0; i < 2; ++i) {
     void* ptr = i == 0 ? (void*)hi : (void*)ho;
     cudaPointerAttributes at{};
     if (cudaPointerGetAttributes(&at, ptr) == cudaSuccess && at.type == cudaMemoryTypeHost) continue;  // caller-pinned
     cudaGetLastError();
     cudaError_t er = cudaHostRegister(ptr, bytes, cudaHostRegisterDefault);
+    if (er != cudaSuccess && er != cudaErrorHostMemoryAlreadyRegistered && i == 0) {
+      // read-only pages (e.g. a read-only mapping of the input file): step 1
+      // gathers its blocks through pinned staging buffers instead
+      cudaGetLastError();
+      staged_in = true;
+      continue;
+    }
     if (er == cudaSuccess) r.reg[i] = ptr;
     else if (er == cudaErrorHostMemoryAlreadyRegistered) cudaGetLastError();  // caller-pinned: keep as is
     else {
@@ -986,6 +998,13 @@ int efft_execute_outofcore(int64_t n, int dtype, int direction, int device, uint
       return fail(EFFT_ERR_ALLOC, "out-of-core device buffers (4 x %zu bytes)", buf);
     }
     CUDA_TRY(cudaStreamCreateWithFlags(&r.s[i], cudaStreamNonBlocking));
+    if (staged_in) {
+      if (cudaHostAlloc(&r.stage[i], (size_t)(n1 * cb) * e, cudaHostAllocDefault) != cudaSuccess) {
+        cudaGetLastError();
+        return fail(EFFT_ERR_ALLOC, "out-of-core pinned staging (2 x %zu bytes)", (size_t)(n1 * cb) * e);
+      }
+      CUDA_TRY(cudaEventCreateWithFlags(&r.ev[i], cudaEventDisableTiming));
+    }
     rc = efft_plan_create_columns(&r.p1[i], n1, cb, dtype, direction, device, 0, 0, pf);
     if (rc != EFFT_OK) return rc;
     rc = efft_plan_create_columns(&r.p2[i], n2, rb, dtype, direction, device, n, 0, pf);
@@ -994,7 +1013,15 @@ int efft_execute_outofcore(int64_t n, int dtype, int direction, int device, uint
   // step 1
   for (int64_t c0 = 0, k = 0; c0 < n2; c0 += cb, ++k) {
     const int i = (int)(k & 1);
-    CUDA_TRY(cudaMemcpy2DAsync(r.a[i], cb * e, hi + c0 * e, n2 * e, cb * e, n1, cudaMemcpyHostToDevice, r.s[i]));
+    if (staged_in) {  // host gather of block k overlaps the device work of block k-1
+      if (k >= 2) CUDA_TRY(cudaEventSynchronize(r.ev[i]));
+      char* st = (char*)r.stage[i];
+      for (int64_t row = 0; row < n1; ++row) memcpy(st + row * cb * e, hi + (row * n2 + c0) * e, cb * e);
+      CUDA_TRY(cudaMemcpyAsync(r.a[i], st, (size_t)(n1 * cb) * e, cudaMemcpyHostToDevice, r.s[i]));
+      CUDA_TRY(cudaEventRecord(r.ev[i], r.s[i]));
+    } else {
+      CUDA_TRY(cudaMemcpy2DAsync(r.a[i], cb * e, hi + c0 * e, n2 * e, cb * e, n1, cudaMemcpyHostToDevice, r.s[i]));
+    }
     rc = efft_execute(r.p1[i], r.a[i], r.a[i], r.s[i]);
     if (rc != EFFT_OK) return rc;
     rc = efft_permute_swap01(r.a[i], r.b[i], n1, cb, 1, (int)e, r.s[i]);  // [k1][c] -> [c][k1]

@@ -68,3 +68,14 @@ def test_out_of_core_rejects_overlap():
     x = random_c(1 << 20, seed=1).astype(np.complex64)
     with pytest.raises(ValueError, match="overlap"):  # EFFT_ERR_INVALID_ARG
         outofcore.transform(x, out=x)
+
+
+def test_out_of_core_read_only_mapped_input(tmp_path):
+    """The input may be a read-only file mapping (the reference reads binary arrays from disk)."""
+    n = 1 << 20
+    x = random_c(n, seed=9).astype(np.complex64)
+    f = tmp_path / "x.c64"
+    x.tofile(f)
+    xm = np.memmap(f, dtype=np.complex64, mode="r", shape=(n,))
+    y = outofcore.transform(xm, device_bytes=1 << 20)
+    assert oracle.rel_l2(y, oracle.transform(x.astype(np.complex128))) <= tol(n, np.complex64)
