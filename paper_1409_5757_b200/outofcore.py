@@ -6,11 +6,13 @@ plan workspace do not fit in HBM, the four-step form runs over host memory
 with bounded device buffers.  With N = N1 N2, x viewed as (N1 x N2) row-major
 (n = n1 N2 + n2) and X[k1 + N1 k2]:
 
-  step 1  for every block of C columns n2:  Y[k1][n2] = sum_n1 x[n1][n2] W_N1^(n1 k1)
-          (gather the block, H2D, a batched column plan, D2H into Y)
-  step 2  for every block of Rr rows k1:    X[k1 + N1 k2] = sum_n2 Y[k1][n2] W_N^(n2 k1) W_N2^(n2 k2)
-          (contiguous rows H2D, device transpose, a column plan with the
-          four-step twiddle on its input, D2H into X viewed as (N2 x N1))
+  step 1  for every block of C columns n2:  Yt[n2][k1] = sum_n1 x[n1][n2] W_N1^(n1 k1)
+          (strided H2D of the block, a batched column plan, a device
+          transpose, contiguous D2H into rows c0.. of Yt, which lives in `out`)
+  step 2  for every block of Rr columns k1:  X[k1 + N1 k2] = sum_n2 Yt[n2][k1] W_N^(n2 k1) W_N2^(n2 k2)
+          (strided H2D of the block, a column plan with the four-step
+          twiddle on its input, strided D2H back into the same columns of
+          `out`, now viewed as X[k2][k1])
 
 The streaming runs natively (efft_execute_outofcore in efft_capi.cu): the
 caller's arrays are page-locked for the call, every block moves by strided
