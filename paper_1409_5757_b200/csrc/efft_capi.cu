@@ -431,11 +431,25 @@ int build_plan(efft_plan_s* pl) {
     R2 = 1;
   } else {
     pl->npass = 2;
-    // balanced split; the factor 3 goes to pass 1
-    int t1 = t / 2;
+    // Beyond two direct passes (n > dmax^2) the first pass is a direct one of
+    // radix M*2^k <= 256 (c128) / 512 (c64) / dmax (M > 1) and the second a
+    // staged one: 1.1-1.9x the balanced two-staged split on B200 from 2^21 to
+    // 2^25 (tools/split_sizes.py, profiles/r01_split_sizes.txt).  Otherwise a
+    // balanced split; the odd factor goes to pass 1.  EFFT_SPLIT_T1 (log2 of
+    // pass 1's power of two) overrides both, for experiments.
+    const int F2 = dt == EFFT_C64 ? 16 : 8;
+    int t1 = env_int("EFFT_SPLIT_T1", -1);
+    PassPlan a, b;
+    if (t1 < 0 && pl->n > dmax * dmax) {
+      const int64_t cap = M == 1 ? (dt == EFFT_C128 ? 256 : 512) : dmax;
+      int k = 0;
+      while (k < t && ((int64_t)M << (k + 1)) <= cap) ++k;
+      const int64_t r1 = (int64_t)M << k, r2 = pl->n / r1;
+      if (pick_pass(dt, r1, &a) && !a.staged && pick_pass(dt, r2, &b) && (!b.staged || r1 % F2 == 0)) t1 = k;
+    }
+    if (t1 < 0 || t1 > t) t1 = t / 2;
     R1 = (int64_t)M << t1;
     R2 = pl->n / R1;
-    PassPlan a, b;
     if (!pick_pass(dt, R1, &a) || !pick_pass(dt, R2, &b)) {
       // shift one power of two between the passes and retry
       bool ok = false;
