@@ -141,7 +141,11 @@ def max_over_ranks(v, world):
 
 
 def cpu_baseline(cfg_name, cfg, x_dev, max_seconds=25.0):
-    """Time the oracle (CPU restatement of the reference algorithm) on a bounded sample."""
+    """Time the oracle (CPU restatement of the reference algorithm) on a bounded
+    sample; returns (cpu_baseline dict, oracle output or None).  The output is
+    the oracle's float32 reference-recipe transform (c64) or fp64 transform
+    (c128) of the WHOLE input when the sample is the whole input -- reused as
+    the full-array parity comparator."""
     import numpy as np
 
     import oracle
@@ -152,15 +156,15 @@ def cpu_baseline(cfg_name, cfg, x_dev, max_seconds=25.0):
     # bounded sample: the largest power-of-two prefix (x 3 for C4) that runs in ~max_seconds
     m = 3 if n_full % 3 == 0 else 1
     n = min(n_full, m << 22)
-    host = x_dev[:n_full].cpu().numpy() if n_full <= (1 << 30) else None
+    host = x_dev[:n_full].cpu().numpy() if n_full <= (3 << 28) else None
     best = None
     while True:
         if host is not None:
-            x = np.ascontiguousarray(host[:n])
+            x = host[:n] if n == n_full else np.ascontiguousarray(host[:n])
         else:
             x = x_dev[:n].cpu().numpy()
         t0 = time.perf_counter()
-        oracle.transform(x, precision=prec, threads=threads)
+        out = oracle.transform(x, precision=prec, threads=threads)
         dt = time.perf_counter() - t0
         best = (n, dt)
         if n >= n_full or dt * 2.3 > max_seconds:
@@ -168,13 +172,112 @@ def cpu_baseline(cfg_name, cfg, x_dev, max_seconds=25.0):
         n *= 2
     n, dt = best
     gflops = 5.0 * n * math.log2(n) / dt / 1e9
-    return {"value": round(gflops, 3), "unit": "GFLOP/s", "cores": threads, "kind": "port",
-            "sample": f"one {prec} transform of N={n} (prefix of {cfg_name}'s N={n_full} input), "
-                      f"{dt:.2f} s, oracle/efft_oracle.c with {threads} OpenMP threads"}
+    kind = ("float32 arithmetic with the reference's twiddle recipe" if prec == "c64"
+            else "fp64 arithmetic")
+    line = {"value": round(gflops, 3), "unit": "GFLOP/s", "cores": threads, "kind": "port",
+            "sample": f"one {prec} transform of N={n} ({'the whole' if n == n_full else 'prefix of'} "
+                      f"{cfg_name}'s N={n_full} input), {dt:.2f} s, oracle/efft_oracle.c "
+                      f"({kind}) with {threads} OpenMP threads",
+            "python_reference_context": PY_REFERENCE_CONTEXT}
+    return line, (out if n == n_full else None), (host if n == n_full else None)
+
+
+# The reference package itself (Python, real float32 two-real composition) is
+# not installable on the GPU box; its own numbers, measured in the build
+# container, are kept beside the C restatement's.
+PY_REFERENCE_CONTEXT = ("reference efft package (Python/numpy, real f32, two-real composition): "
+                        "2.71 GFLOP/s at N=2^30, 2.70 at 2^27, 1.31 at 2^21 on 8 cores "
+                        "(BASELINE.md section 2, build container)")
+
+
+def rel_l2_chunked(a, b, chunk=1 << 26):
+    """Relative L2 of a against b (numpy arrays), fp64 accumulation, bounded temporaries."""
+    import numpy as np
+
+    num = den = 0.0
+    for i in range(0, a.shape[0], chunk):
+        bb = b[i:i + chunk].astype(np.complex128)
+        d = a[i:i + chunk].astype(np.complex128) - bb
+        num += float(np.vdot(d, d).real)
+        den += float(np.vdot(bb, bb).real)
+    return math.sqrt(num / den)
+
+
+def device_rel_l2(a, b, chunk=1 << 26):
+    """Relative L2 of device tensors a against b, fp64 accumulation, chunked."""
+    import torch
+
+    num = den = 0.0
+    for i in range(0, a.numel(), chunk):
+        bb = torch.view_as_real(b[i:i + chunk]).double()
+        d = torch.view_as_real(a[i:i + chunk]).double() - bb
+        num += float(d.pow(2).sum())
+        den += float(bb.pow(2).sum())
+    return math.sqrt(num / den)
+
+
+def parity_report(cfg, x, y, inv_plan, oracle_out, x_host, sid):
+    """Full-array parity of the timed transform's output y = F(x) (north star:
+    rel-L2 <= 1e-5 log2N (c64) / 1e-12 log2N (c128) against the reference CPU
+    path on the same input, round-trip error reported)."""
+    import numpy as np
+    import torch
+
+    import oracle
+
+    n, dtype = cfg["n"], cfg["dtype"]
+    tol = (1e-5 if dtype == "complex64" else 1e-12) * math.log2(n)
+    out = {"tolerance": tol}
+    # forward -> inverse round trip on the device (the inverse plan scales by 1/N)
+    if inv_plan is not None:
+        z = torch.empty_like(x)
+        inv_plan.execute(y.data_ptr(), z.data_ptr(), sid)
+        torch.cuda.synchronize()
+        out["rt_err"] = device_rel_l2(z, x)
+        del z
+    y_host = None
+    try:
+        import psutil
+
+        avail = psutil.virtual_memory().available
+    except Exception:
+        avail = 0
+    elem = 8 if dtype == "complex64" else 16
+    if oracle_out is not None:
+        y_host = y.cpu().numpy()
+        key = "rel_l2_vs_f32_reference_recipe" if dtype == "complex64" else "rel_l2"
+        out[key] = rel_l2_chunked(y_host, oracle_out)
+        out["comparator"] = ("oracle/efft_oracle.c float32 path (the reference's twiddle recipe, "
+                             "recombine.py:49-59) on the whole input" if dtype == "complex64"
+                             else "oracle/efft_oracle.c fp64 restatement on the whole input")
+    if dtype == "complex64" and x_host is not None and avail > n * 40 + (8 << 30):
+        # fp64 restatement of the same complex64 input: the ground truth
+        t0 = time.perf_counter()
+        exact = oracle.transform(x_host.astype(np.complex128), precision="c128")
+        if y_host is None:
+            y_host = y.cpu().numpy()
+        out["rel_l2"] = rel_l2_chunked(y_host, exact)
+        out["comparator_fp64"] = f"oracle fp64 restatement of the same input ({time.perf_counter() - t0:.1f} s)"
+        del exact
+    elif "rel_l2" not in out and oracle_out is None:
+        out["rel_l2"] = None
+        out["note"] = (f"full-array oracle skipped: {n * elem * 2 >> 30} GiB of host arrays "
+                       f"(tests/test_gpu_parity.py checks this config by spots, Parseval and round trip)")
+    ok = all(v is None or v <= (2 * tol if k == "rt_err" else tol)
+             for k, v in out.items() if k.startswith("rel_l2") or k == "rt_err")
+    out["within_tolerance"] = ok
+    for k in list(out):
+        if isinstance(out[k], float) and k != "tolerance":
+            out[k] = float(f"{out[k]:.4e}")
+    return out
 
 
 def run_reference(args):
-    """--impl reference: the CPU restatement of the reference path, rank 0 only."""
+    """--impl reference: the CPU restatement of the reference path (oracle/,
+    C + OpenMP on all host cores), rank 0 only, on the SAME config as our arm:
+    each step is one transform (C2/C5: forward + inverse) of the config's full N
+    on the same seeded input (generated on the GPU when one is present, as our
+    arm does, then copied to the host outside the timed region)."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
@@ -186,11 +289,32 @@ def run_reference(args):
     cfg = workloads.CONFIGS[args.config]
     prec = "c64" if cfg["dtype"] == "complex64" else "c128"
     threads = oracle.host_threads()
-    m = 3 if cfg["n"] % 3 == 0 else 1
-    n = min(cfg["n"], m << 24)  # bounded sample per step (~1-3 s on 16 cores)
-    rng = np.random.default_rng(workloads.seed_for(args.config))
-    x = (rng.standard_normal(n) + 1j * rng.standard_normal(n)).astype(
-        np.complex64 if prec == "c64" else np.complex128)
+    n = cfg["n"]
+    elem = 8 if prec == "c64" else 16
+    try:
+        import psutil
+
+        avail = psutil.virtual_memory().available
+    except Exception:
+        avail = 1 << 62
+    same = True
+    if 2 * n * elem + (4 << 30) > avail:  # C5 (2 x 64 GiB) on a small host: largest pow2 prefix that fits
+        same = False
+        while 2 * n * elem + (4 << 30) > avail and n > (1 << 20):
+            n //= 2
+    seed = workloads.seed_for(args.config)
+    try:
+        import torch
+
+        if not torch.cuda.is_available():
+            raise RuntimeError
+        x = workloads.make_input(cfg["n"], cfg["dtype"], cfg["kind"], seed)[:n].cpu().numpy()
+        gen = "workloads.make_input (torch CUDA generator, same seed as our arm), copied to the host"
+    except Exception:
+        rng = np.random.default_rng(seed)
+        x = (rng.standard_normal(n) + 1j * rng.standard_normal(n)).astype(
+            np.complex64 if prec == "c64" else np.complex128)
+        gen = "numpy default_rng(seed) N(0,1) (no GPU visible: same distribution, different values)"
     out = np.empty_like(x)
     per_step = 2 if cfg["roundtrip"] else 1
     for _ in range(args.warmup):
@@ -203,19 +327,23 @@ def run_reference(args):
     dt = time.perf_counter() - t0
     flops = 5.0 * n * math.log2(n) * per_step * args.steps
     gflops = flops / dt / 1e9
+    what = f"{per_step} {prec} transform(s) of N={n}" + ("" if same else f" (host RAM caps the full N={cfg['n']})")
     line = {
         "impl": "reference", "metric": "GFLOP/s (5N*log2N) per 1D FFT",
         "value": round(gflops, 3), "unit": "GFLOP/s", "n_gpus": args.gpus, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(dt / args.steps * 1e3, 3),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": DTYPE_NAME[cfg["dtype"]], "data": "synthetic",
-        "config": {"workload": f"{args.config}: {cfg['dtype']} 1D DFT, N={cfg['n']}",
-                   "sample_n": n, "roundtrip": cfg["roundtrip"]},
+        "config": {"workload": f"{args.config}: {'forward+inverse' if cfg['roundtrip'] else 'forward'} "
+                               f"1D {cfg['dtype']} DFT, N={cfg['n']}",
+                   "n": n, "same_config": same, "input": gen, "roundtrip": cfg["roundtrip"]},
         "cpu_baseline": {"value": round(gflops, 3), "unit": "GFLOP/s", "cores": threads,
                          "kind": "port",
-                         "sample": f"each step = {per_step} {prec} transform(s) of N={n} (bounded "
-                                   f"sample of N={cfg['n']}); oracle/efft_oracle.c, the C restatement "
-                                   f"of the reference EFFT algorithm (reference is Python-only)"},
+                         "sample": f"each step = {what}; oracle/efft_oracle.c, the C restatement of the "
+                                   f"reference EFFT algorithm ({'float32 with the reference twiddle recipe' if prec == 'c64' else 'fp64'}), "
+                                   f"{threads} OpenMP threads (the reference is Python-only and cannot travel "
+                                   f"to the GPU box)",
+                         "python_reference_context": PY_REFERENCE_CONTEXT},
         "e2e": {"value": round(gflops, 3), "unit": "GFLOP/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
@@ -311,9 +439,12 @@ def run_ours(args):
     x = workloads.make_input(n, dtype, cfg["kind"], seed, device="cuda")
     y = torch.empty_like(x)
     ndt = _native.EFFT_C64 if dtype == "complex64" else _native.EFFT_C128
-    fwd = _native.NativePlan(n, ndt, -1, local)
-    inv = _native.NativePlan(n, ndt, 1, local) if cfg["roundtrip"] else None
-    fwd.enable_timing(True)
+    # the flags the drop-in handle uses (core.TransformHandle): the non-finite
+    # input check of the reference's scatter (scatter.py:38-39) is timed too
+    flags = _native.EFFT_FLAG_CHECK_FINITE
+    fwd = _native.NativePlan(n, ndt, -1, local, flags)
+    inv = _native.NativePlan(n, ndt, 1, local, flags | _native.EFFT_FLAG_SCALE_INVERSE)
+    fwd.enable_timing(args.steps)  # per-launch events of every timed step (averaged)
     stream = torch.cuda.current_stream()
     sid = stream.cuda_stream
     per_step = 2 if cfg["roundtrip"] else 1
@@ -322,14 +453,14 @@ def run_ours(args):
 
     def step():
         fwd.execute(x.data_ptr(), y.data_ptr(), sid)
-        if inv is not None:
+        if cfg["roundtrip"]:
             inv.execute(y.data_ptr(), x.data_ptr(), sid)
 
     for _ in range(max(args.warmup, 3)):
         step()
     torch.cuda.synchronize()
-    launches = fwd.launches() + (inv.launches() if inv else 0)
-    pass_ms = [[] for _ in range(fwd.launches())]
+    launches = fwd.launches() + (inv.launches() if cfg["roundtrip"] else 0)
+    fwd.enable_timing(args.steps)  # drop the warm-up executions
     barrier(world)
     torch.cuda.synchronize()
     with ClockSampler(local) as clocks:
@@ -343,9 +474,6 @@ def run_ours(args):
             e1.record()
             torch.cuda.synchronize()
             total_ms = e0.elapsed_time(e1)
-            # per-launch durations of the last step (events on the launching stream)
-            for k, v in enumerate(fwd.launch_times_ms()):
-                pass_ms[k].append(v)
         else:
             total_ms = 0.0
             for _ in range(args.steps):
@@ -356,8 +484,6 @@ def run_ours(args):
                 e1.record()
                 torch.cuda.synchronize()
                 total_ms += e0.elapsed_time(e1)
-                for k, v in enumerate(fwd.launch_times_ms()):
-                    pass_ms[k].append(v)
     torch.cuda.synchronize()
     barrier(world)
     total_ms = max_over_ranks(total_ms, world)
@@ -367,7 +493,8 @@ def run_ours(args):
 
     # dominant kernel roofline (pass kernels move 2*N*elem algorithmic bytes each)
     peak, peak_src = measured_peaks()
-    avg = [sum(v) / len(v) for v in pass_ms if v]
+    # per-launch durations averaged over every timed step (events on the launching stream)
+    avg = fwd.launch_times_ms()
     dom = max(range(len(avg)), key=lambda k: avg[k])
     alg_bytes = 2 * n * ELEM[dtype]
     achieved = alg_bytes / (avg[dom] * 1e-3) / 1e9
@@ -417,7 +544,7 @@ def run_ours(args):
         torch.cuda.synchronize()
         barrier(world)
         t0 = time.perf_counter()
-        if inv is None:
+        if not cfg["roundtrip"]:
             # pipelined: transform k+1's H2D overlaps transform k's passes + D2H
             fwd.execute_host_batch([hin.data_ptr()] * e2e_steps, [hout.data_ptr()] * e2e_steps, sid)
         else:
@@ -433,14 +560,22 @@ def run_ours(args):
                "d2h_bytes_per_step": per_step * n * ELEM[dtype],
                "ms_per_step": round(dt / e2e_steps * 1e3, 3),
                "path": ("efft_execute_host_batch (C ABI): per transform pinned host -> H2D -> passes -> D2H "
-                        "-> host, consecutive transforms overlapped (H2D of k+1 with D2H of k)") if inv is None
+                        "-> host, consecutive transforms overlapped (H2D of k+1 with D2H of k)") if not cfg["roundtrip"]
                        else ("efft_execute_host_batch (C ABI) of the forward plan, then of the inverse plan: "
                              "per transform pinned host -> H2D -> passes -> D2H -> host, overlapped")}
         del hin, hout
 
     cpu = None
+    oracle_out = host_in = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        cpu = cpu_baseline(args.config, cfg, x if x_host is None else x_host)
+        cpu, oracle_out, host_in = cpu_baseline(args.config, cfg, x if x_host is None else x_host)
+    parity = None
+    if rank == 0 and not args.no_parity and x_host is None:
+        if cfg["roundtrip"]:  # x was overwritten by the timed inverse: y = F(x) holds again
+            fwd.execute(x.data_ptr(), y.data_ptr(), sid)
+            torch.cuda.synchronize()
+        parity = parity_report(cfg, x, y, inv, oracle_out, host_in, sid)
+    del oracle_out, host_in
 
     if rank == 0:
         line = {
@@ -466,6 +601,7 @@ def run_ours(args):
             "clocks": clocks.summary(),
             "e2e": e2e,
             "cpu_baseline": cpu,
+            "parity": parity,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -484,9 +620,18 @@ def main():
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--no-e2e", action="store_true", help="skip the host-buffer e2e leg")
     ap.add_argument("--e2e-steps", type=int, default=8)
+    ap.add_argument("--no-parity", action="store_true", help="skip the full-array parity leg")
     ap.add_argument("--replicas", action="store_true",
                     help="N>1: independent per-GPU transforms instead of one sharded transform")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # one process per GPU: launch the ranks ourselves (the driver uses torchrun directly)
+        import subprocess
+
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr", "127.0.0.1", "--master-port", os.environ.get("MASTER_PORT", "29533"),
+               os.path.abspath(__file__)] + sys.argv[1:]
+        sys.exit(subprocess.call(cmd))
     if args.impl == "reference":
         run_reference(args)
     else:

@@ -92,7 +92,9 @@ int efft_execute_host(efft_plan_t plan, const void *h_in, void *h_out, void *str
  * stream while transform k computes and copies back on `stream`, so both PCIe
  * directions are busy at once (two device in/out pairs from the per-device
  * pool, kept for later calls; one at a time when the second pair does not fit).
- * Returns after the last copy-back has completed. */
+ * Returns after the last copy-back has completed.  Transform k+1's input is
+ * read once transform k-1's output has landed, so h_in[j] must not alias any
+ * h_out[i] with i >= j - 1 (chained transforms: issue them as separate calls). */
 int efft_execute_host_batch(efft_plan_t plan, const void *const *h_in, void *const *h_out, int count,
                             void *stream);
 
@@ -122,9 +124,10 @@ int efft_nonfinite_seen(efft_plan_t plan, int *seen, void *stream);
 int efft_plan_destroy(efft_plan_t plan);
 
 /* Per-launch device timing (CUDA events recorded on the execution stream
- * around every kernel the plan launches).  Enable once; after an execution
- * has completed, efft_plan_launch_times() fills ms[0..launches-1] with the
- * durations of the most recent execution. */
+ * around every kernel the plan launches).  enable = K > 0 keeps the events of
+ * the last K executions (a ring; 0 switches timing off and drops them); once
+ * those executions have completed, efft_plan_launch_times() fills
+ * ms[0..launches-1] with each launch's duration averaged over them. */
 int efft_plan_enable_timing(efft_plan_t plan, int enable);
 int efft_plan_launch_times(efft_plan_t plan, float *ms, int max_launches);
 

@@ -189,8 +189,9 @@ class NativePlan:
         check(load().efft_nonfinite_seen(self._h, ctypes.byref(v), stream))
         return bool(v.value)
 
-    def enable_timing(self, on: bool = True) -> None:
-        check(load().efft_plan_enable_timing(self._h, 1 if on else 0))
+    def enable_timing(self, on=True) -> None:
+        """on: False/0 off, True = the last execution, int K = average over the last K."""
+        check(load().efft_plan_enable_timing(self._h, int(on)))
 
     def launch_times_ms(self) -> list:
         n = self.launches()

@@ -203,13 +203,18 @@ class TransformHandle:
         torch = _torch()
         with torch.cuda.device(self.plan.device):
             stream = torch.cuda.current_stream()
+            # read-and-clear: a flag left by run_device / execute_* on other data
+            # must not reject this input
+            self._native.nonfinite_seen(stream.cuda_stream)
             self._dev_in.copy_(self._host_in, non_blocking=True)
             self._native.execute(self._dev_in.data_ptr(), self._dev_out.data_ptr(),
                                  stream.cuda_stream)
-            self._host_out.copy_(self._dev_out, non_blocking=True)
-            stream.synchronize()
+            # the reference rejects the input before writing any output
+            # (scatter.py:38-39): check before the copy-back, result untouched
             if self._native.nonfinite_seen(stream.cuda_stream):
                 raise ValueError("input contains non-finite values")
+            self._host_out.copy_(self._dev_out, non_blocking=True)
+            stream.synchronize()
         return self._result
 
     def close(self) -> None:
@@ -265,6 +270,13 @@ class TransformHandle:
         torch = _torch()
         if h_in.shape != (self.plan.n,) or h_out.shape != (self.plan.n,):
             raise SizeMismatch(f"host buffers must have length {self.plan.n}")
+        want = self._data.dtype
+        if h_in.dtype != want or h_out.dtype != want:
+            raise SizeMismatch(f"host buffers must be {want} (the plan dtype)")
+        if not (h_in.flags.c_contiguous and h_out.flags.c_contiguous):
+            raise SizeMismatch("host buffers must be C-contiguous")
+        if not h_out.flags.writeable:
+            raise SizeMismatch("h_out must be writable")
         with torch.cuda.device(self.plan.device):
             s = torch.cuda.current_stream()
             self._native.execute_host(h_in.ctypes.data, h_out.ctypes.data, s.cuda_stream)

@@ -20,6 +20,7 @@
 #include <algorithm>
 #include <cstring>
 #include <mutex>
+#include <vector>
 #include <string>
 
 #include "../../include/efft_b200.h"
@@ -137,7 +138,10 @@ struct efft_plan_s {
   int32_t* flag = nullptr;
   int num_sms = 0;
   bool timing = false;
-  cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};  // launch boundaries
+  // launch boundaries of the last `tcap` executes (4 events each), a ring
+  std::vector<cudaEvent_t> tev;
+  int tcap = 0;
+  long long tcount = 0;
   // lean path (lean.cu): large M * 2^t transforms (both dtypes)
   bool lean = false;
   efft::lean::Pass lp[2];
@@ -771,8 +775,10 @@ int efft_execute(efft_plan_t pl, const void* d_in, void* d_out, void* stream) {
   cudaStream_t s = (cudaStream_t)stream;
   CUDA_TRY(cudaSetDevice(pl->device));
   CUDA_TRY(cudaMemsetAsync(pl->counters, 0, pl->counter_bytes, s));
+  cudaEvent_t* ev = pl->timing ? &pl->tev[(size_t)(pl->tcount % pl->tcap) * 4] : nullptr;
+  if (pl->timing) ++pl->tcount;
   for (int p = 0; pl->lean && p < 2; ++p) {
-    if (pl->timing) CUDA_TRY(cudaEventRecord(pl->ev[p], s));
+    if (ev) CUDA_TRY(cudaEventRecord(ev[p], s));
     efft::lean::Pass& q = pl->lp[p];
     efft::lean::Args a = q.a;
     a.src = p == 0 ? d_in : d_out;
@@ -781,7 +787,7 @@ int efft_execute(efft_plan_t pl, const void* d_in, void* d_out, void* stream) {
     CUDA_TRY(cudaGetLastError());
   }
   for (int p = 0; !pl->lean && p < pl->npass; ++p) {
-    if (pl->timing) CUDA_TRY(cudaEventRecord(pl->ev[p], s));
+    if (ev) CUDA_TRY(cudaEventRecord(ev[p], s));
     PassPlan& pp = pl->pass[p];
     const void* src = p == 0 ? d_in : d_out;
     if (pp.k.ws && pp.tmA_ptr != src) {
@@ -794,12 +800,12 @@ int efft_execute(efft_plan_t pl, const void* d_in, void* d_out, void* stream) {
     pp.k.fn<<<pp.grid, pp.k.nt, pp.k.smem_bytes, s>>>(a);
     CUDA_TRY(cudaGetLastError());
   }
-  if (pl->timing) CUDA_TRY(cudaEventRecord(pl->ev[pl->npass], s));
+  if (ev) CUDA_TRY(cudaEventRecord(ev[pl->npass], s));
   if (pl->real_input) {
     const int64_t h = pl->n, work = h / 2 + 1;
     real_split_kernel<<<(unsigned)((work + 255) / 256), 256, 0, s>>>((float2*)d_out, h, pl->n_user);
     CUDA_TRY(cudaGetLastError());
-    if (pl->timing) CUDA_TRY(cudaEventRecord(pl->ev[pl->npass + 1], s));
+    if (ev) CUDA_TRY(cudaEventRecord(ev[pl->npass + 1], s));
   }
   return EFFT_OK;
 }
@@ -1043,6 +1049,14 @@ int efft_execute_outofcore(int64_t n, int dtype, int direction, int device, uint
     CUDA_TRY(cudaMemcpyAsync(ho + c0 * n1 * e, r.b[i], cb * n1 * e, cudaMemcpyDeviceToHost, r.s[i]));
   }
   for (int i = 0; i < 2; ++i) CUDA_TRY(cudaStreamSynchronize(r.s[i]));
+  if (pf & EFFT_FLAG_CHECK_FINITE) {  // the reference rejects non-finite input (scatter.py:38-39)
+    for (int i = 0; i < 2; ++i) {
+      int seen = 0;
+      rc = efft_nonfinite_seen(r.p1[i], &seen, r.s[i]);
+      if (rc != EFFT_OK) return rc;
+      if (seen) return fail(EFFT_ERR_INVALID_ARG, "input contains non-finite values");
+    }
+  }
   // step 2 (the twiddle offset of a column plan is the first k1 of its block)
   for (int64_t r0 = 0, k = 0; r0 < n1; r0 += rb, ++k) {
     const int i = (int)(k & 1);
@@ -1086,27 +1100,45 @@ int efft_nonfinite_seen(efft_plan_t pl, int* seen, void* stream) {
 
 int efft_plan_enable_timing(efft_plan_t pl, int enable) {
   if (!pl) return fail(EFFT_ERR_INVALID_ARG, "NULL plan");
+  if (enable < 0) return fail(EFFT_ERR_INVALID_ARG, "enable must be >= 0, got %d", enable);
   CUDA_TRY(cudaSetDevice(pl->device));
-  if (enable && !pl->ev[0])
-    for (auto& e : pl->ev) CUDA_TRY(cudaEventCreate(&e));
-  pl->timing = enable != 0;
+  for (auto& e : pl->tev)
+    if (e) cudaEventDestroy(e);
+  pl->tev.clear();
+  pl->tcap = enable;
+  pl->tcount = 0;
+  pl->timing = enable > 0;
+  if (pl->timing) {
+    pl->tev.assign((size_t)enable * 4, nullptr);
+    for (auto& e : pl->tev) CUDA_TRY(cudaEventCreate(&e));
+  }
   return EFFT_OK;
 }
 
 int efft_plan_launch_times(efft_plan_t pl, float* ms, int max_launches) {
   if (!pl || !ms) return fail(EFFT_ERR_INVALID_ARG, "NULL argument");
   if (!pl->timing) return fail(EFFT_ERR_INVALID_ARG, "timing not enabled");
+  if (pl->tcount == 0) return fail(EFFT_ERR_INVALID_ARG, "no timed execute yet");
   const int nl = pl->npass + (pl->real_input ? 1 : 0);
+  const long long first = pl->tcount > pl->tcap ? pl->tcount - pl->tcap : 0;
   CUDA_TRY(cudaSetDevice(pl->device));
-  for (int i = 0; i < nl && i < max_launches; ++i)
-    CUDA_TRY(cudaEventElapsedTime(&ms[i], pl->ev[i], pl->ev[i + 1]));
+  for (int i = 0; i < nl && i < max_launches; ++i) {
+    double sum = 0;
+    for (long long j = first; j < pl->tcount; ++j) {
+      const cudaEvent_t* ev = &pl->tev[(size_t)(j % pl->tcap) * 4];
+      float t = 0;
+      CUDA_TRY(cudaEventElapsedTime(&t, ev[i], ev[i + 1]));
+      sum += t;
+    }
+    ms[i] = (float)(sum / (double)(pl->tcount - first));
+  }
   return EFFT_OK;
 }
 
 int efft_plan_destroy(efft_plan_t pl) {
   if (!pl) return EFFT_OK;
   cudaSetDevice(pl->device);
-  for (auto& e : pl->ev)
+  for (auto& e : pl->tev)
     if (e) cudaEventDestroy(e);
   if (pl->staging) cudaFree(pl->staging);
   if (pl->counters) cudaFree(pl->counters);

@@ -11,7 +11,7 @@ from typing import Optional
 
 from .errors import MissingBaseline, NonPositiveSize
 
-CSV_HEADER = "size,splits,workers,runtime_s,gflops,l2,mem_bytes,status,gbps,roofline_frac,ngpus,dtype"
+CSV_HEADER = "size,splits,workers,runtime_s,gflops,l2,mem_bytes,status,gbps,roofline_frac,ngpus,dtype,rt_err"
 
 
 def flops_model(n: int, complex_input: bool = False) -> float:
@@ -48,6 +48,7 @@ class RunMetrics:
     roofline_frac: Optional[float] = None
     ngpus: int = 1
     dtype: str = "complex64"
+    rt_err: Optional[float] = None  # forward -> inverse round-trip relative L2 (north star)
 
     @classmethod
     def from_timing(cls, n, splits, workers, wall_seconds, complex_input=True, **kw):
@@ -60,4 +61,5 @@ class RunMetrics:
         f = lambda v, fmt: "" if v is None else format(v, fmt)  # noqa: E731
         return (f"{self.n},{self.splits},{self.workers},{self.wall_seconds:.6e},{self.gflops:.6g},"
                 f"{f(self.l2, '.6e')},{f(self.peak_mem_bytes, 'd')},{self.status},"
-                f"{f(self.gbps, '.6g')},{f(self.roofline_frac, '.4f')},{self.ngpus},{self.dtype}")
+                f"{f(self.gbps, '.6g')},{f(self.roofline_frac, '.4f')},{self.ngpus},{self.dtype},"
+                f"{f(self.rt_err, '.6e')}")

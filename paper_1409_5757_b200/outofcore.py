@@ -88,7 +88,8 @@ def transform(x: np.ndarray, direction: int = -1, device: int = 0, device_bytes:
     if res.dtype != x.dtype or res.shape != (n,) or not res.flags.c_contiguous:
         raise ValueError("out must be a contiguous array like x")
     ndt = _native.EFFT_C64 if dtype == "complex64" else _native.EFFT_C128
-    flags = _native.EFFT_FLAG_SCALE_INVERSE if direction == 1 else 0
+    # non-finite input is rejected like the in-core handle (reference scatter.py:38-39)
+    flags = _native.EFFT_FLAG_CHECK_FINITE | (_native.EFFT_FLAG_SCALE_INVERSE if direction == 1 else 0)
     _native.execute_outofcore(n, ndt, direction, device, flags, x.ctypes.data, res.ctypes.data, device_bytes)
     return res
 

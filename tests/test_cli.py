@@ -27,7 +27,7 @@ def test_parse_int_list():
 def test_csv_header_extends_reference_schema():
     ref = "size,splits,workers,runtime_s,gflops,l2,mem_bytes,status"  # reference bench.py:21
     assert CSV_HEADER.startswith(ref)
-    assert CSV_HEADER.split(",")[len(ref.split(",")):] == ["gbps", "roofline_frac", "ngpus", "dtype"]
+    assert CSV_HEADER.split(",")[len(ref.split(",")):] == ["gbps", "roofline_frac", "ngpus", "dtype", "rt_err"]
     assert len(cli._failed(16, 2, 1, "complex64").split(",")) == len(CSV_HEADER.split(","))
 
 

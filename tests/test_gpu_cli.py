@@ -63,3 +63,17 @@ def test_transform_out_of_core_option(tmp_path, capsys):
     y = np.fromfile(dst, dtype=np.complex128)
     ref = np.fft.fft(x)
     assert np.linalg.norm(y - ref) / np.linalg.norm(ref) < 1e-12
+
+
+@pytest.mark.parametrize("dtype", ["float32", "complex64"])
+def test_check_corrupt_fails_like_the_reference(dtype, capsys):
+    """reference cli.py:125-150: --corrupt perturbs the result; status failed, exit 1"""
+    assert cli.main(["check", "--size", "2^12", "--splits", "2", "--dtype", dtype, "--corrupt"]) == 1
+    (r,) = rows(capsys.readouterr().out)
+    assert r["status"] == "failed"
+
+
+def test_check_reports_roundtrip_error(capsys):
+    assert cli.main(["check", "--size", "2^20", "--splits", "3", "--dtype", "complex128"]) == 0
+    (r,) = rows(capsys.readouterr().out)
+    assert 0 <= float(r["rt_err"]) < 1e-13

@@ -45,7 +45,10 @@ SIZES = [2, 4, 8, 16, 32, 64, 128, 256, 512, 1024, 3, 6, 12, 24, 48, 96, 192, 38
          # radix-5 / radix-7 families: direct tiles, two direct
          # passes, staged rho_a = 320 / 448
          5, 10, 40, 160, 320, 640, 5 * 2 ** 10, 5 * 2 ** 14, 5 * 2 ** 16, 5 * 2 ** 19,
-         7, 28, 112, 448, 896, 7 * 2 ** 10, 7 * 2 ** 15, 7 * 2 ** 17, 7 * 2 ** 19]
+         7, 28, 112, 448, 896, 7 * 2 ** 10, 7 * 2 ** 15, 7 * 2 ** 17, 7 * 2 ** 19,
+         # generic two-pass plans above dmax^2 (direct M*2^k pass 1 + staged pass 2,
+         # c128 rho_b up to 512 at 2^25) and the radix-M families in that range
+         2 ** 22, 2 ** 23, 2 ** 24, 2 ** 25, 3 * 2 ** 21, 3 * 2 ** 23, 5 * 2 ** 21, 7 * 2 ** 21]
 
 
 @pytest.mark.parametrize("dtype", ["complex64", "complex128"])

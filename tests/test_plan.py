@@ -98,7 +98,7 @@ class TestMetrics:
         assert algorithmic_bytes(2 ** 30, 8, 2) == 2 * 2 * 2 ** 30 * 8
         m = RunMetrics.from_timing(2 ** 20, 0, 1, 0.5)
         assert m.gflops == pytest.approx(5 * 2 ** 20 * 20 / 0.5 / 1e9)
-        assert len(m.csv_row().split(",")) == 12
+        assert len(m.csv_row().split(",")) == 13
         assert efficiency({1: 2.0, 2: 3.0})[2] == pytest.approx(0.75)
         with pytest.raises(errors.MissingBaseline):
             efficiency({2: 1.0})

@@ -29,9 +29,14 @@ if len(sys.argv) > 1:  # child: one (n, dtype, t1)
         torch.cuda.synchronize()
         ts.append(e0.elapsed_time(e1))
     ts.sort()
+    # every timed split must also be right: rel-L2 against torch's fp64 FFT
+    ref = torch.fft.fft(x.to(torch.complex128))
+    err = (torch.linalg.vector_norm(y.to(torch.complex128) - ref) / torch.linalg.vector_norm(ref)).item()
+    lg = max(1.0, float(torch.tensor(float(n)).log2()))
+    assert err <= (1e-12 if dt == "c128" else 1e-5) * lg, (n, dt, os.environ.get("EFFT_SPLIT_T1"), err)
     plan = [l.split(" grid")[0] for l in p.describe().splitlines()[1:]]
     print(json.dumps({"n": n, "dtype": dt, "t1": os.environ.get("EFFT_SPLIT_T1", "default"),
-                      "ms_median": round(ts[len(ts) // 2], 4), "plan": plan}))
+                      "ms_median": round(ts[len(ts) // 2], 4), "rel_l2": err, "plan": plan}))
     sys.exit(0)
 
 cases = [(1 << 21, "c128"), (1 << 23, "c128"), (1 << 25, "c128"), (3 << 20, "c128"), (5 << 20, "c128"),
