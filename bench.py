@@ -156,7 +156,8 @@ def cpu_baseline(cfg_name, cfg, x_dev, max_seconds=25.0):
     # bounded sample: the largest power-of-two prefix (x 3 for C4) that runs in ~max_seconds
     m = 3 if n_full % 3 == 0 else 1
     n = min(n_full, m << 22)
-    host = x_dev[:n_full].cpu().numpy() if n_full <= (3 << 28) else None
+    elem = 8 if prec == "c64" else 16
+    host = x_dev[:n_full].cpu().numpy() if n_full * elem <= (16 << 30) else None
     best = None
     while True:
         if host is not None:

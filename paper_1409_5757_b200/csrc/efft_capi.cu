@@ -26,6 +26,7 @@
 #include "../../include/efft_b200.h"
 #include "efft_registry.cuh"
 #include "lean.cuh"
+#include "tpass.cuh"
 
 using efft::KernelInfo;
 using efft::PassArgs;
@@ -145,7 +146,9 @@ struct efft_plan_s {
   // lean path (lean.cu): large M * 2^t transforms (both dtypes)
   bool lean = false;
   efft::lean::Pass lp[2];
-  void* lean_t4 = nullptr;  // pass-1 four-step twiddle tables (48 / 96 KB)
+  // TMA-pipelined path (tpass.cu): complex64 N = 2^30
+  bool tp = false;
+  efft::tpass::Pass tpp[2];
 };
 
 namespace {
@@ -406,6 +409,15 @@ int build_plan(efft_plan_s* pl) {
   if (!pl->columns && env_int("EFFT_LEAN", 1)) {
     int64_t stg = 0;
     int ecuda = 0;
+    if (efft::tpass::plan(pl->n, dt == EFFT_C128, pl->direction == EFFT_INVERSE,
+                          (pl->flags & EFFT_FLAG_CHECK_FINITE) != 0, pl->num_sms, pl->tpp, &stg, &ecuda)) {
+      pl->tp = true;
+      pl->npass = 2;
+      pl->staging_bytes = (size_t)stg * pl->elem;
+      pl->counter_bytes = (size_t)(pl->tpp[0].counter_ints + pl->tpp[1].counter_ints) * 4;
+      return EFFT_OK;
+    }
+    if (ecuda) return fail(EFFT_ERR_CUDA, "TMA pass setup failed: %s", cudaGetErrorString(cudaGetLastError()));
     if (efft::lean::plan(pl->n, dt == EFFT_C128, pl->direction == EFFT_INVERSE, true,
                          (pl->flags & EFFT_FLAG_CHECK_FINITE) != 0, pl->num_sms, pl->lp, &stg, &ecuda)) {
       pl->lean = true;
@@ -558,18 +570,23 @@ int finish_plan(efft_plan_s* pl) {
     g_err = keep;
     return rc;
   }
+  if (pl->tp) {
+    int64_t off = 0;
+    for (auto& q : pl->tpp) {
+      q.a.stg = pl->staging;
+      q.a.ctr = reinterpret_cast<unsigned long long*>(pl->counters + off);
+      q.a.doneA = pl->counters + off + 2;
+      q.a.doneB = q.a.doneA + q.a.ngroups;
+      q.a.flag = pl->flag;
+      off += q.counter_ints;
+    }
+    if (efft::tpass::encode_ring(pl->tpp[0], pl->staging) != 0) {
+      efft_plan_destroy(pl);
+      return fail(EFFT_ERR_CUDA, "tensor map (TMA pass ring) encode failed");
+    }
+    return EFFT_OK;
+  }
   if (pl->lean) {
-    if (cudaMalloc(&pl->lean_t4, efft::lean::table_bytes(pl->dtype == EFFT_C128)) != cudaSuccess) {
-      cudaGetLastError();
-      efft_plan_destroy(pl);
-      return fail(EFFT_ERR_ALLOC, "lean twiddle tables");
-    }
-    efft::lean::build_tables(pl->lean_t4, pl->n, pl->dtype == EFFT_C128, 0);
-    if (cudaDeviceSynchronize() != cudaSuccess) {
-      efft_plan_destroy(pl);
-      return fail(EFFT_ERR_CUDA, "lean twiddle tables: %s", cudaGetErrorString(cudaGetLastError()));
-    }
-    pl->lp[0].a.t4 = pl->lean_t4;
     int64_t off = 0;
     for (auto& q : pl->lp) {
       q.a.stg = pl->staging;
@@ -722,6 +739,15 @@ int efft_plan_describe(efft_plan_t pl, char* buf, size_t len) {
            (long long)pl->n, pl->dtype == EFFT_C64 ? "c64" : "c128", pl->direction, pl->npass,
            pl->staging_bytes);
   s += line;
+  for (int p = 0; pl->tp && p < 2; ++p) {
+    const efft::tpass::Pass& q = pl->tpp[p];
+    snprintf(line, sizeof line,
+             "pass %d: R=%lld tma staged rho_a=256 rho_b=%d stages=[16x16 | 8x16] F=32 grid=%d x %d smem=%d "
+             "groups=%d tasks=%lld lag=%d slots=%d\n",
+             p, (long long)q.a.R, q.rb, q.grid, q.nt, q.smem, q.a.ngroups, (long long)q.a.total, q.a.lag,
+             q.a.nslots);
+    s += line;
+  }
   for (int p = 0; pl->lean && p < 2; ++p) {
     const efft::lean::Pass& q = pl->lp[p];
     snprintf(line, sizeof line,
@@ -732,7 +758,7 @@ int efft_plan_describe(efft_plan_t pl, char* buf, size_t len) {
              q.a.lag, q.a.nslots);
     s += line;
   }
-  for (int p = 0; !pl->lean && p < pl->npass; ++p) {
+  for (int p = 0; !pl->lean && !pl->tp && p < pl->npass; ++p) {
     const PassPlan& pp = pl->pass[p];
     std::string st;
     for (int i = 0; i < pp.k.nst_a; ++i) st += (i ? "x" : "") + std::to_string(pp.k.stages_a[i]);
@@ -777,6 +803,43 @@ int efft_execute(efft_plan_t pl, const void* d_in, void* d_out, void* stream) {
   CUDA_TRY(cudaMemsetAsync(pl->counters, 0, pl->counter_bytes, s));
   cudaEvent_t* ev = pl->timing ? &pl->tev[(size_t)(pl->tcount % pl->tcap) * 4] : nullptr;
   if (pl->timing) ++pl->tcount;
+  for (int p = 0; pl->tp && p < 2; ++p) {
+    if (ev) CUDA_TRY(cudaEventRecord(ev[p], s));
+    efft::tpass::Pass& q = pl->tpp[p];
+    const void* src = p == 0 ? d_in : d_out;
+    if (q.mapA_ptr != src && efft::tpass::encode_input(q, p, src) != 0)
+      return fail(EFFT_ERR_CUDA, "tensor map (TMA pass input) encode failed");
+    efft::tpass::Args a = q.a;
+    a.src = src;
+    a.dst = d_out;
+    static const bool tprof = getenv("EFFT_TP_PROF") != nullptr;
+    if (tprof) {  // diagnostics: per-phase cycle sums of this launch, printed to stderr
+      static unsigned long long* buf = nullptr;
+      if (!buf) CUDA_TRY(cudaMalloc(&buf, 96 * 8));
+      CUDA_TRY(cudaMemsetAsync(buf, 0, 96 * 8, s));
+      a.prof = buf;
+      q.fn_prof<<<q.grid, q.nt, q.smem, s>>>(a);
+      CUDA_TRY(cudaGetLastError());
+      unsigned long long h[96];
+      CUDA_TRY(cudaMemcpyAsync(h, buf, sizeof h, cudaMemcpyDeviceToHost, s));
+      CUDA_TRY(cudaStreamSynchronize(s));
+      const double ctas = q.grid;
+      fprintf(stderr,
+              "tpass pass %d (per CTA): producer dep-wait %.0f, buffer-wait %.0f, total %.0f cycles; "
+              "deferred %.1f of %.1f tiles; compute warp 0: tile-wait %.0f, barrier %.0f, total %.0f\n",
+              p, h[0] / ctas, h[1] / ctas, h[2] / ctas, h[6] / ctas, h[7] / ctas, h[3] / ctas, h[4] / ctas,
+              (double)h[5] / ctas);
+      for (int k = 0; k < 2; ++k) {
+        fprintf(stderr, "  compute warp 0 %s tiles, cycles per tile [ld, st0, bar+sts+bar, ld1, st1+stores, end]:",
+                k ? "B" : "A");
+        for (int i = 0; i < 6; ++i) fprintf(stderr, " %.0f", h[8 + k * 6 + i] / ctas / (h[7] / ctas / 2));
+        fprintf(stderr, "\n");
+      }
+      continue;
+    }
+    q.fn<<<q.grid, q.nt, q.smem, s>>>(a);
+    CUDA_TRY(cudaGetLastError());
+  }
   for (int p = 0; pl->lean && p < 2; ++p) {
     if (ev) CUDA_TRY(cudaEventRecord(ev[p], s));
     efft::lean::Pass& q = pl->lp[p];
@@ -786,7 +849,7 @@ int efft_execute(efft_plan_t pl, const void* d_in, void* d_out, void* stream) {
     q.fn<<<q.grid, q.nt, q.smem, s>>>(a);
     CUDA_TRY(cudaGetLastError());
   }
-  for (int p = 0; !pl->lean && p < pl->npass; ++p) {
+  for (int p = 0; !pl->lean && !pl->tp && p < pl->npass; ++p) {
     if (ev) CUDA_TRY(cudaEventRecord(ev[p], s));
     PassPlan& pp = pl->pass[p];
     const void* src = p == 0 ? d_in : d_out;
@@ -1143,7 +1206,6 @@ int efft_plan_destroy(efft_plan_t pl) {
   if (pl->staging) cudaFree(pl->staging);
   if (pl->counters) cudaFree(pl->counters);
   if (pl->flag) cudaFree(pl->flag);
-  if (pl->lean_t4) cudaFree(pl->lean_t4);
   delete pl;
   return EFFT_OK;
 }

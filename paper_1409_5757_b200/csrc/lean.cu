@@ -17,9 +17,10 @@
 //     sub-stage; the transposing exchange uses padded rows so both sides are
 //     bank-conflict free;
 //   * radix-16 / 12 / QB register DFTs (paired-fp32 FADD2/FFMA2 for c64);
-//   * twiddles from fp64-built tables (W_256 and W_R^(i<256) in shared memory,
-//     three 2048-entry levels of W_N in a 48/96 KB plan buffer) with short
-//     recurrences: no N-sized twiddle array is read.
+//   * twiddles: W_256 and W_R^(i<256) in shared memory (built per CTA in fp64,
+//     rounded once); the pass-1 four-step twiddle W_N^(j2 k1) from the exact
+//     integer exponent -- fp64 sincospi base and step, fp64 recurrence, one
+//     rounding per use.  No global twiddle table is read.
 //
 // Index maps (N = R1 R2, R = RA RB per pass, j = ja + RB jb, k = kb + RA ka,
 // jb = s + A1 t, kb = kt + A0 ks (RA = A0 A1: 16 x 16, or 12 / 10 / 14 x 16
@@ -88,12 +89,6 @@ __device__ __forceinline__ float2 cscale(float2 v, float2 c) { return mul2(v, c)
 __device__ __forceinline__ double2 cscale(double2 v, double2 c) { return make_double2(v.x * c.x, v.y * c.y); }
 __device__ __forceinline__ float2 cvt(double2 c, float) { return make_float2((float)c.x, (float)c.y); }
 __device__ __forceinline__ double2 cvt(double2 c, double) { return c; }
-
-// W_N^e, e < N <= 2^32: three 11-bit levels
-template <typename V>
-__device__ __forceinline__ V w_full(const V* t4, uint32_t e) {
-  return cmul(cmul(__ldg(t4 + (e >> 22)), __ldg(t4 + 2048 + ((e >> 11) & 2047))), __ldg(t4 + 4096 + (e & 2047)));
-}
 
 // Position -> (sub-stage, group, task) of the claim order above (thread 0 only).
 __device__ __forceinline__ void decode(const Args& a, uint32_t pos, int& isB, int& g, int& task) {
@@ -286,7 +281,6 @@ __global__ void __launch_bounds__(LT<R>::NT, MINB) lean_pass(const __grid_consta
 #define SRC reinterpret_cast<const V*>(a.src)
 #define DST reinterpret_cast<V*>(a.dst)
 #define STG reinterpret_cast<V*>(a.stg)
-#define T4 reinterpret_cast<const V*>(a.t4)
   for (int i = tid; i < 256; i += NT) {
     w256[i] = to_v(wroot(i, 256), R());
     wlo[i] = to_v(wroot(i, a.R), R());
@@ -400,12 +394,14 @@ __global__ void __launch_bounds__(LT<R>::NT, MINB) lean_pass(const __grid_consta
         t1_task<F, S>(task, ks, h, jblk);
         const int j2 = g * F + jblk * DB + dl;
         const uint32_t c = (uint32_t)(h * F + lane + 16 * ks + RA * kq);
-        V w = w_full(T4, (uint32_t)((uint64_t)j2 * c));
-        const V st = w_full(T4, (uint32_t)(((uint64_t)j2 * (RA * QB)) % (uint64_t)a.N));
+        // W_N^(j2 k1) from the exact integer exponent: fp64 base and step
+        // (sincospi), fp64 recurrence, one rounding per use (north star c)
+        double2 w = wroot((int64_t)(((uint64_t)j2 * c) % (uint64_t)a.N), a.N);
+        const double2 st = wroot((int64_t)(((uint64_t)j2 * (RA * QB)) % (uint64_t)a.N), a.N);
         V* op = DST + (int64_t)j2 * a.R + c;
 #pragma unroll
         for (int kp = 0; kp < 16; ++kp) {
-          st_hint(op + kp * (RA * QB), cmul(v[P<16>(kp)], w), pol);
+          st_hint(op + kp * (RA * QB), cmul(v[P<16>(kp)], to_v(w, R())), pol);
           if (kp < 15) w = cmul(w, st);
         }
       } else {
@@ -435,7 +431,6 @@ __global__ void __launch_bounds__(LT<R>::NT, MINB) lean_pass(const __grid_consta
 #undef SRC
 #undef DST
 #undef STG
-#undef T4
 }
 
 // Paired-column complex64 tile kernel (the default for complex64, RA = 256):
@@ -493,7 +488,6 @@ __global__ void __launch_bounds__(pair::NT, 4) lean_pair(const __grid_constant__
 #define SRC reinterpret_cast<const V*>(a.src)
 #define DST reinterpret_cast<V*>(a.dst)
 #define STG reinterpret_cast<V*>(a.stg)
-#define T4 reinterpret_cast<const V*>(a.t4)
   for (int i = tid; i < 256; i += pair::NT) {
     w256[i] = to_v(wroot(i, 256), 0.f);
     wlo[i] = to_v(wroot(i, a.R), 0.f);
@@ -642,14 +636,20 @@ __global__ void __launch_bounds__(pair::NT, 4) lean_pair(const __grid_constant__
         // y[k1 + R1 j2] = Y W_N^(j2 k1), k1 = kt + 16 ks + 256 kq + 256 QB kp, kt = 2cp (+1)
         const int j2 = g * 16 + (task >> 4) * DB + dl;
         const uint32_t c = (uint32_t)(2 * cp + 16 * (task & 15) + 256 * kq);
-        V w = w_full(T4, (uint32_t)((uint64_t)j2 * c));
-        const V w1 = w_full(T4, (uint32_t)j2);  // W_N^j2: column kt + 1
-        const V st = w_full(T4, (uint32_t)(((uint64_t)j2 * (256 * QB)) % (uint64_t)a.N));
+        // W_N^(j2 k1) for columns kt and kt + 1 from exact integer exponents:
+        // fp64 bases and step (sincospi), fp64 recurrence, one rounding per
+        // use -- fp64-accurate twiddles on the fp32 path, no table (north star c)
+        // (column kt + 1: times W_N^j2 in fp32, <= 1.5 ulp)
+        const uint64_t N = (uint64_t)a.N;
+        double2 w0 = wroot((int64_t)(((uint64_t)j2 * c) % N), a.N);
+        const V wj = to_v(wroot((int64_t)((uint64_t)j2 % N), a.N), 0.f);
+        const double2 st = wroot((int64_t)(((uint64_t)j2 * (256 * QB)) % N), a.N);
         V* op = DST + (int64_t)j2 * a.R + c;
 #pragma unroll
         for (int kp = 0; kp < 16; ++kp) {
-          pair::st16(op + kp * (256 * QB), cmul(x[P<16>(kp)], w), cmul(y[P<16>(kp)], cmul(w, w1)), pol);
-          if (kp < 15) w = cmul(w, st);
+          const V w = to_v(w0, 0.f);
+          pair::st16(op + kp * (256 * QB), cmul(x[P<16>(kp)], w), cmul(y[P<16>(kp)], cmul(w, wj)), pol);
+          if (kp < 15) w0 = cmul(w0, st);
         }
       } else {
         const int kb = task * DB + dl;
@@ -688,30 +688,11 @@ __global__ void __launch_bounds__(pair::NT, 4) lean_pair(const __grid_constant__
 #undef SRC
 #undef DST
 #undef STG
-#undef T4
-}
-
-template <typename R>
-__global__ void tables_kernel(typename CT<R>::V* t4, int64_t n) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= 3 * 2048) return;
-  const int lvl = i >> 11, j = i & 2047;
-  const uint64_t ex = ((uint64_t)j << (11 * (2 - lvl))) % (uint64_t)n;
-  t4[i] = to_v(wroot((int64_t)ex, n), R());
 }
 
 // ---------------------------------------------------------------------------
 // host side
 // ---------------------------------------------------------------------------
-size_t table_bytes(int c128) { return (size_t)3 * 2048 * (c128 ? 16 : 8); }
-
-void build_tables(void* t4, int64_t n, int c128, cudaStream_t s) {
-  if (c128)
-    tables_kernel<double><<<24, 256, 0, s>>>((double2*)t4, n);
-  else
-    tables_kernel<float><<<24, 256, 0, s>>>((float2*)t4, n);
-}
-
 template <typename R, int RA>
 static void* pick_ra(int rb, bool t1) {
   if constexpr (RA != 256) {  // the odd factor runs in the in-place pass only

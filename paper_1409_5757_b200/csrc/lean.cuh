@@ -24,7 +24,6 @@ struct Args {
   const void* src;
   void* dst;
   void* stg;
-  const void* t4;      // pass 1: W_N^(i << 22), W_N^(i << 11), W_N^i, i < 2048 (plan buffer, fp64-built)
   int64_t LS;          // element stride between successive DFT points in src
   int64_t R;           // DFT length of the pass (256 * RB)
   int64_t N;           // full transform length (four-step twiddle of pass 1)
@@ -53,10 +52,6 @@ struct Pass {
 // (err_cuda set when a CUDA call failed).  Reports the staging elements needed.
 bool plan(int64_t n, int c128, int inverse, bool scale_inverse, bool check_finite, int num_sms, Pass p[2],
           int64_t* staging_elems, int* err_cuda);
-
-// Pass-1 four-step twiddle tables (3 x 2048 elements of the plan's type).
-size_t table_bytes(int c128);
-void build_tables(void* t4, int64_t n, int c128, cudaStream_t s);
 
 }  // namespace lean
 }  // namespace efft

@@ -221,6 +221,54 @@ __global__ void __launch_bounds__(256, 1) k_staged(const __grid_constant__ KP p)
   if (p.mode == 2 && tid == 0) bulk_wait_read<0>();
 }
 
+// ---------------------------------------------------------------- register-staged, 1-deep prefetch
+// The tpass structure: one 64 KB landing buffer per CTA (TMA box {32, 256}),
+// tile -> registers (32 x 8 B per thread), barrier, next TMA issued, then a
+// synthetic compute delay of `delay` cycles and the stores (contiguous).
+__global__ void __launch_bounds__(256, 2) k_regs(const __grid_constant__ KP p, int delay, int nbuf) {
+  extern __shared__ __align__(1024) unsigned char sm[];
+  __shared__ uint64_t bar[2];
+  const int tid = threadIdx.x;
+  constexpr int TBY = 65536;
+  const int64_t RB_PER = ROWS / 256;
+  const uint64_t pf = pol_first();
+  if (tid == 0) {
+    mb_init(&bar[0], 1);
+    mb_init(&bar[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const int64_t my0 = blockIdx.x, step = gridDim.x;
+  const int64_t ntiles = N * 8 / TBY;
+  const int64_t nmine = (ntiles - my0 + step - 1) / step;
+  auto issue = [&](int64_t k) {
+    const int64_t t = my0 + k * step;
+    const int b = (int)(k % nbuf);
+    const int64_t cg = t / RB_PER, rb = t % RB_PER;
+    mb_expect(&bar[b], TBY);
+    tma2d(sm + (size_t)b * TBY, &p.in, (int)(cg * 32), (int)(rb * 256), &bar[b], pf);
+  };
+  if (tid == 0) for (int k = 0; k < nbuf - 1 && k < nmine; ++k) issue(k);
+  for (int64_t k = 0; k < nmine; ++k) {
+    const int b = (int)(k % nbuf);
+    if (tid == 0 && nbuf == 1) issue(k);
+    mb_wait(&bar[b], (uint32_t)((k / nbuf) & 1));
+    uint4 v[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) v[i] = lds16(sm + (size_t)b * TBY + (i * 256 + tid) * 16);
+    __syncthreads();
+    if (tid == 0 && nbuf > 1 && k + nbuf - 1 < nmine) issue(k + nbuf - 1);
+    if (delay > 0) {
+      const long long t0 = clock64();
+      while (clock64() - t0 < delay) {
+      }
+    }
+    const int64_t t = my0 + k * step;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) stg16(p.dst + t * TBY + (i * 256 + tid) * 16, v[i], pf);
+  }
+}
+
 // ---------------------------------------------------------------- cluster / DSMEM skeleton
 // Cluster of C CTAs handles one group of F columns x ROWS (=2^15) rows at a time:
 // CTA c loads rows [c*ROWS/C, (c+1)*ROWS/C) (boxes of 256 rows) into buffer b,
@@ -448,6 +496,24 @@ int main(int argc, char** argv) {
   }
   if (want("ring")) { staged(4, 16, "ring", S3{}, 1); staged(4, 16, "ring", S3{}, 4); }
 
+  if (want("regs")) {
+    KP p;
+    memset(&p, 0, sizeof(p));
+    p.in = map2d(src, 32, 256);
+    p.src = src;
+    p.dst = dst;
+    for (int nbuf : {1, 2}) {
+      const int smem = nbuf * 65536;
+      CK(cudaFuncSetAttribute(k_regs, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+      int occ = 0;
+      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_regs, 256, smem));
+      for (int delay : {0, 1000, 2000, 4000, 6000}) {
+        char nm[64];
+        snprintf(nm, sizeof nm, "regs nbuf=%d occ=%d delay=%d", nbuf, occ, delay);
+        report(nm, timeit([&] { k_regs<<<sms * occ, 256, smem>>>(p, delay, nbuf); }));
+      }
+    }
+  }
   if (want("dsm")) {
     struct Cfg { int C, F, NB; };
     for (Cfg c : {Cfg{8, 4, 3}, Cfg{16, 4, 3}, Cfg{16, 8, 1}, Cfg{8, 8, 1}, Cfg{16, 4, 2}, Cfg{8, 4, 2}, Cfg{16, 2, 4}}) {
