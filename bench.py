@@ -393,9 +393,10 @@ def run_sharded(args, rank, local, world):
     elem = ELEM[dtype]
     exch = sharded.ShardedTransform.exchanged_bytes(n, world, elem)
     peak, peak_src = measured_peaks()
-    # additive roofline of one sharded transform per rank: 2 FFT passes + 3 local
-    # permutations over HBM, plus 3 all-to-alls over NVLink (770 GB/s measured peer BW)
-    hbm_bytes = 5 * 2 * shard * elem
+    # additive roofline of one sharded transform per rank: the local HBM passes
+    # (2 FFT passes + pack + unpack) plus 3 all-to-alls over NVLink (770 GB/s
+    # measured peer BW); the north-star minimum is 2 local passes
+    hbm_bytes = sharded.ShardedTransform.local_passes() * 2 * shard * elem
     t_roof = hbm_bytes / (peak * 1e9) + exch / 770e9
     if rank == 0:
         line = {

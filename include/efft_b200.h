@@ -142,6 +142,33 @@ int efft_plan_launch_times(efft_plan_t plan, float *ms, int max_launches);
 int efft_plan_create_columns(efft_plan_t *plan, int64_t len, int64_t cols, int dtype, int direction,
                              int device, int64_t tw_mod, int64_t tw_offset, uint32_t flags);
 
+/* Sharded six-step over G = ngpus devices of ONE process (
+ * the reference's only parallelism is the in-process fork-join of
+ * parallel.py:34-98 / recombine.py:263-295).  Natural-order block shards:
+ * rank q (device devices[q]) holds x[q N/G, (q+1) N/G) in in[q] and receives
+ * X[q N/G, (q+1) N/G) in out[q].  N = N1 N2 (efft_sharded_split); per rank two
+ * local HBM passes (the lean pass kernels: pass 1 with the four-step twiddle
+ * and the transpose fused into its store, pass 2 in place in a plan-owned work
+ * array) and three exchanges done as pitched peer copies over NVLink (no
+ * pack / unpack / transpose kernels), ordered by cross-device events on the
+ * callers' streams (streams[q] on devices[q]).  A device may appear more than
+ * once (emulated ranks on one GPU).  Inverse scaled by 1/N.  in[] is not
+ * modified. */
+int efft_plan_create_sharded(efft_plan_t *plan, int64_t n, int dtype, int direction, int ngpus, const int *devices,
+                             uint32_t flags);
+int efft_execute_sharded(efft_plan_t plan, const void *const *in, void *const *out, void *const *streams);
+int efft_sharded_split(efft_plan_t plan, int64_t *n1, int64_t *n2);
+
+/* The same six-step with one process per GPU (torch.distributed / NCCL
+ * drives the exchanges; paper_1409_5757_b200/sharded.py): rank `rank` of
+ * `ngpus` on `device`.  Pass 0: B[n1][c] (N1 x L2, global column rank L2 + c)
+ * -> Y blocked by destination rank [p][c][k1'] (the all-to-all send buffer) with
+ * the four-step twiddle fused; pass 1: T[n2][k1'] (N2 x L1) -> X[k2][k1'] in
+ * place (inverse: 1/N).  Asynchronous on `stream`. */
+int efft_plan_create_shard_rank(efft_plan_t *plan, int64_t n, int dtype, int direction, int ngpus, int rank,
+                                int device, uint32_t flags);
+int efft_execute_shard_pass(efft_plan_t plan, int pass, const void *in, void *out, void *stream);
+
 /* Block permutations (all-to-all packing): shapes (n0, n1, n2) of 8- or
  * 16-byte elements.  swap01: out[b][a][c] = in[a][b][c];  swap12:
  * out[a][c][b] = in[a][b][c].  Asynchronous on `stream`; in != out. */

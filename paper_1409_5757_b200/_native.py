@@ -53,6 +53,11 @@ EXPORTED = (
     "efft_permute_swap01",
     "efft_permute_swap12",
     "efft_plan_launch_times",
+    "efft_plan_create_sharded",
+    "efft_execute_sharded",
+    "efft_sharded_split",
+    "efft_plan_create_shard_rank",
+    "efft_execute_shard_pass",
     "efft_last_error",
     "efft_version",
 )
@@ -91,6 +96,11 @@ def load():
     lib.efft_permute_swap01.argtypes = [vp, vp, i64, i64, i64, i32, vp]
     lib.efft_permute_swap12.argtypes = [vp, vp, i64, i64, i64, i32, vp]
     lib.efft_plan_launch_times.argtypes = [vp, ctypes.POINTER(ctypes.c_float), i32]
+    lib.efft_plan_create_sharded.argtypes = [ctypes.POINTER(vp), i64, i32, i32, i32, ctypes.POINTER(i32), u32]
+    lib.efft_execute_sharded.argtypes = [vp, ctypes.POINTER(vp), ctypes.POINTER(vp), ctypes.POINTER(vp)]
+    lib.efft_sharded_split.argtypes = [vp, ctypes.POINTER(i64), ctypes.POINTER(i64)]
+    lib.efft_plan_create_shard_rank.argtypes = [ctypes.POINTER(vp), i64, i32, i32, i32, i32, i32, u32]
+    lib.efft_execute_shard_pass.argtypes = [vp, i32, vp, vp, vp]
     lib.efft_last_error.restype = ctypes.c_char_p
     lib.efft_last_error.argtypes = []
     lib.efft_version.argtypes = []
@@ -209,3 +219,76 @@ class NativePlan:
             self.close()
         except Exception:
             pass
+
+
+class ShardedPlan:
+    """One efft_plan_create_sharded plan: the six-step over G devices of this
+    process (device ids may repeat: emulated ranks on one GPU)."""
+
+    def __init__(self, n: int, dtype: int, direction: int, devices, flags: int = 0):
+        lib = load()
+        h = ctypes.c_void_p()
+        devs = (ctypes.c_int * len(devices))(*devices)
+        check(lib.efft_plan_create_sharded(ctypes.byref(h), n, dtype, direction, len(devices), devs, flags),
+              "efft_plan_create_sharded")
+        self._h = h
+        self.n, self.dtype, self.direction, self.devices = n, dtype, direction, list(devices)
+
+    def split(self):
+        a, b = ctypes.c_int64(), ctypes.c_int64()
+        check(load().efft_sharded_split(self._h, ctypes.byref(a), ctypes.byref(b)))
+        return a.value, b.value
+
+    def workspace_bytes(self) -> int:
+        v = ctypes.c_size_t()
+        check(load().efft_plan_workspace_bytes(self._h, ctypes.byref(v)))
+        return v.value
+
+    def execute(self, d_in: list, d_out: list, streams: list) -> None:
+        g = len(self.devices)
+        if not (len(d_in) == len(d_out) == len(streams) == g):
+            raise ValueError(f"need {g} input, output and stream pointers")
+        arr = lambda v: (ctypes.c_void_p * g)(*v)  # noqa: E731
+        check(load().efft_execute_sharded(self._h, arr(d_in), arr(d_out), arr(streams)), "efft_execute_sharded")
+
+    def close(self) -> None:
+        if self._h:
+            load().efft_plan_destroy(self._h)
+            self._h = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class ShardRankPlan:
+    """One rank's local passes of the sharded six-step (efft_plan_create_shard_rank)."""
+
+    def __init__(self, n: int, dtype: int, direction: int, world: int, rank: int, device: int, flags: int = 0):
+        lib = load()
+        h = ctypes.c_void_p()
+        check(lib.efft_plan_create_shard_rank(ctypes.byref(h), n, dtype, direction, world, rank, device, flags),
+              "efft_plan_create_shard_rank")
+        self._h = h
+
+    def split(self):
+        a, b = ctypes.c_int64(), ctypes.c_int64()
+        check(load().efft_sharded_split(self._h, ctypes.byref(a), ctypes.byref(b)))
+        return a.value, b.value
+
+    def execute_pass(self, which: int, d_in: int, d_out: int, stream: int) -> None:
+        check(load().efft_execute_shard_pass(self._h, which, d_in, d_out, stream), "efft_execute_shard_pass")
+
+    def close(self) -> None:
+        if self._h:
+            load().efft_plan_destroy(self._h)
+            self._h = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+

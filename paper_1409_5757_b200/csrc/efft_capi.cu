@@ -149,6 +149,20 @@ struct efft_plan_s {
   // TMA-pipelined path (tpass.cu): complex64 N = 2^30
   bool tp = false;
   efft::tpass::Pass tpp[2];
+  // sharded six-step over G devices (efft_plan_create_sharded)
+  struct Rank {
+    int dev = 0;
+    efft::lean::Pass lp[2];
+    void* staging = nullptr;
+    int32_t* counters = nullptr;
+    size_t counter_bytes = 0;
+    int32_t* flag = nullptr;
+    void* work = nullptr;  // N / G elements
+    cudaEvent_t ev = nullptr;
+  };
+  std::vector<Rank> ranks;
+  int64_t sh_n1 = 0, sh_n2 = 0;
+  int sh_rank = 0, sh_world = 0;  // shard-rank plans (efft_plan_create_shard_rank)
 };
 
 namespace {
@@ -781,6 +795,11 @@ int efft_plan_describe(efft_plan_t pl, char* buf, size_t len) {
 int efft_plan_workspace_bytes(efft_plan_t pl, size_t* bytes) {
   if (!pl || !bytes) return fail(EFFT_ERR_INVALID_ARG, "NULL argument");
   *bytes = pl->staging_bytes + pl->counter_bytes + 4;
+  for (const auto& r : pl->ranks)  // sharded: per rank, work array + ring + counters
+    *bytes += (size_t)(pl->n / (int64_t)pl->ranks.size()) * pl->elem +
+              (size_t)std::max(r.lp[0].a.nslots * r.lp[0].a.slot_elems, r.lp[1].a.nslots * r.lp[1].a.slot_elems) *
+                  pl->elem +
+              r.counter_bytes + 4;
   return EFFT_OK;
 }
 
@@ -1198,8 +1217,250 @@ int efft_plan_launch_times(efft_plan_t pl, float* ms, int max_launches) {
   return EFFT_OK;
 }
 
+static int launch_lean(efft::lean::Pass& q, const void* src, void* dst, cudaStream_t s) {
+  efft::lean::Args a = q.a;
+  a.src = src;
+  a.dst = dst;
+  q.fn<<<q.grid, q.nt, q.smem, s>>>(a);
+  CUDA_TRY(cudaGetLastError());
+  return EFFT_OK;
+}
+
+int efft_plan_create_sharded(efft_plan_t* out, int64_t n, int dtype, int direction, int ngpus, const int* devices,
+                             uint32_t flags) {
+  if (!out) return fail(EFFT_ERR_INVALID_ARG, "plan pointer is NULL");
+  *out = nullptr;
+  if (dtype != EFFT_C64 && dtype != EFFT_C128) return fail(EFFT_ERR_INVALID_ARG, "dtype %d (complex only)", dtype);
+  if (direction != EFFT_FORWARD && direction != EFFT_INVERSE)
+    return fail(EFFT_ERR_INVALID_ARG, "direction must be -1 or +1, got %d", direction);
+  if (ngpus < 1 || ngpus > 64 || (ngpus & (ngpus - 1)) || !devices)
+    return fail(EFFT_ERR_INVALID_ARG, "ngpus must be a power of two in [1, 64] with a device list");
+  const int c128 = dtype == EFFT_C128;
+  int64_t N1, N2;
+  if (!efft::lean::split_sharded(n, ngpus, c128, &N1, &N2))
+    return fail(EFFT_ERR_UNSUPPORTED_SIZE, "n=%lld cannot be sharded over %d GPUs (N = N1 N2 with N1 = 2^a >= 2^12, "
+                "N2 = M 2^b, G F | N1, N2)", (long long)n, ngpus);
+  int ndev = 0;
+  CUDA_TRY(cudaGetDeviceCount(&ndev));
+  for (int i = 0; i < ngpus; ++i)
+    if (devices[i] < 0 || devices[i] >= ndev) return fail(EFFT_ERR_INVALID_ARG, "device %d of %d", devices[i], ndev);
+  efft_plan_s* pl = new efft_plan_s();
+  pl->n = pl->n_user = n;
+  pl->dtype = dtype;
+  pl->direction = direction;
+  pl->device = devices[0];
+  pl->flags = flags;
+  pl->elem = c128 ? 16 : 8;
+  pl->npass = 2;
+  pl->sh_n1 = N1;
+  pl->sh_n2 = N2;
+  pl->ranks.resize(ngpus);
+  const size_t local = (size_t)(n / ngpus) * pl->elem;
+  for (int q = 0; q < ngpus; ++q) {
+    auto& r = pl->ranks[q];
+    r.dev = devices[q];
+    if (cudaSetDevice(r.dev) != cudaSuccess) {
+      efft_plan_destroy(pl);
+      return fail(EFFT_ERR_CUDA, "cudaSetDevice(%d)", r.dev);
+    }
+    int sms = 0, ecuda = 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, r.dev);
+    int64_t stg = 0;
+    if (!efft::lean::plan_sharded(n, ngpus, q, c128, direction == EFFT_INVERSE, (flags & EFFT_FLAG_CHECK_FINITE) != 0,
+                                  sms, r.lp, &stg, &ecuda)) {
+      efft_plan_destroy(pl);
+      return ecuda ? fail(EFFT_ERR_CUDA, "sharded pass setup failed") : fail(EFFT_ERR_UNSUPPORTED_SIZE, "no pass kernel");
+    }
+    r.counter_bytes = (size_t)(r.lp[0].counter_ints + r.lp[1].counter_ints) * 4;
+    if (cudaMalloc(&r.staging, (size_t)stg * pl->elem) != cudaSuccess ||
+        cudaMalloc((void**)&r.counters, r.counter_bytes) != cudaSuccess || cudaMalloc((void**)&r.flag, 4) != cudaSuccess ||
+        cudaMalloc(&r.work, local) != cudaSuccess || cudaMemset(r.flag, 0, 4) != cudaSuccess ||
+        cudaEventCreateWithFlags(&r.ev, cudaEventDisableTiming) != cudaSuccess) {
+      cudaGetLastError();
+      efft_plan_destroy(pl);
+      return fail(EFFT_ERR_ALLOC, "sharded rank %d buffers (%zu bytes + ring)", q, local);
+    }
+    int64_t off = 0;
+    for (auto& ps : r.lp) {
+      ps.a.stg = r.staging;
+      ps.a.ctr = reinterpret_cast<unsigned long long*>(r.counters + off);
+      ps.a.doneA = r.counters + off + 2;
+      ps.a.doneB = ps.a.doneA + ps.a.ngroups;
+      ps.a.flag = r.flag;
+      off += ps.counter_ints;
+    }
+    // peer access to every other device (the exchanges are pitched peer copies)
+    for (int p = 0; p < ngpus; ++p) {
+      if (devices[p] == r.dev) continue;
+      int can = 0;
+      cudaDeviceCanAccessPeer(&can, r.dev, devices[p]);
+      if (can) {
+        cudaError_t e = cudaDeviceEnablePeerAccess(devices[p], 0);
+        if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) {
+          cudaGetLastError();
+          efft_plan_destroy(pl);
+          return fail(EFFT_ERR_CUDA, "peer access %d -> %d: %s", r.dev, devices[p], cudaGetErrorString(e));
+        }
+        cudaGetLastError();
+      }
+    }
+  }
+  *out = pl;
+  return EFFT_OK;
+}
+
+int efft_execute_sharded(efft_plan_t pl, const void* const* in, void* const* out, void* const* streams) {
+  if (!pl || !in || !out || !streams) return fail(EFFT_ERR_INVALID_ARG, "NULL argument");
+  if (pl->ranks.empty()) return fail(EFFT_ERR_INVALID_ARG, "not a sharded plan");
+  const int G = (int)pl->ranks.size();
+  const int64_t N1 = pl->sh_n1, N2 = pl->sh_n2, L1 = N1 / G, L2 = N2 / G;
+  const size_t e = pl->elem;
+  for (int q = 0; q < G; ++q)
+    if (!in[q] || !out[q] || in[q] == out[q]) return fail(EFFT_ERR_INVALID_ARG, "rank %d: bad buffers", q);
+  auto S = [&](int q) { return (cudaStream_t)streams[q]; };
+  auto W = [&](int q) { return (char*)pl->ranks[q].work; };
+  // every rank's stream waits for every rank's previous step (cross-device events)
+  auto all_wait = [&]() -> int {
+    for (int q = 0; q < G; ++q) {
+      CUDA_TRY(cudaSetDevice(pl->ranks[q].dev));
+      CUDA_TRY(cudaEventRecord(pl->ranks[q].ev, S(q)));
+    }
+    for (int q = 0; q < G; ++q) {
+      CUDA_TRY(cudaSetDevice(pl->ranks[q].dev));
+      for (int p = 0; p < G; ++p)
+        if (p != q) CUDA_TRY(cudaStreamWaitEvent(S(q), pl->ranks[p].ev, 0));
+    }
+    return EFFT_OK;
+  };
+  int rc = all_wait();
+  if (rc != EFFT_OK) return rc;
+  // exchange 1 (pulled by the destination): B_q[p L1 + r][c] = x_p[r][q L2 + c]
+  for (int q = 0; q < G; ++q) {
+    CUDA_TRY(cudaSetDevice(pl->ranks[q].dev));
+    for (int p = 0; p < G; ++p)
+      CUDA_TRY(cudaMemcpy2DAsync(W(q) + (size_t)(p * L1 * L2) * e, L2 * e, (const char*)in[p] + (size_t)(q * L2) * e,
+                                 N2 * e, L2 * e, L1, cudaMemcpyDefault, S(q)));
+    // pass 1: B_q -> Y'_q[c][k1] (in out_q), twiddle W_N^((q L2 + c) k1)
+    CUDA_TRY(cudaMemsetAsync(pl->ranks[q].counters, 0, pl->ranks[q].counter_bytes, S(q)));
+    rc = launch_lean(pl->ranks[q].lp[0], W(q), out[q], S(q));
+    if (rc != EFFT_OK) return rc;
+  }
+  rc = all_wait();
+  if (rc != EFFT_OK) return rc;
+  // exchange 2: T_p[q L2 + c][k1'] = Y'_q[c][p L1 + k1']; pass 2 in place on T_p
+  for (int p = 0; p < G; ++p) {
+    CUDA_TRY(cudaSetDevice(pl->ranks[p].dev));
+    for (int q = 0; q < G; ++q)
+      CUDA_TRY(cudaMemcpy2DAsync(W(p) + (size_t)(q * L2 * L1) * e, L1 * e, (const char*)out[q] + (size_t)(p * L1) * e,
+                                 N1 * e, L1 * e, L2, cudaMemcpyDefault, S(p)));
+    rc = launch_lean(pl->ranks[p].lp[1], W(p), W(p), S(p));
+    if (rc != EFFT_OK) return rc;
+  }
+  rc = all_wait();
+  if (rc != EFFT_OK) return rc;
+  // exchange 3: y_r[k2'][p L1 + k1'] = X_p[r L2 + k2'][k1'] (natural-order output blocks)
+  for (int r = 0; r < G; ++r) {
+    CUDA_TRY(cudaSetDevice(pl->ranks[r].dev));
+    for (int p = 0; p < G; ++p)
+      CUDA_TRY(cudaMemcpy2DAsync((char*)out[r] + (size_t)(p * L1) * e, N1 * e, W(p) + (size_t)(r * L2 * L1) * e,
+                                 L1 * e, L1 * e, L2, cudaMemcpyDefault, S(r)));
+  }
+  // the exchange-3 sources (work arrays) are reused by the next call only
+  // after every rank's stream has passed this point
+  return all_wait();
+}
+
+int efft_plan_create_shard_rank(efft_plan_t* out, int64_t n, int dtype, int direction, int ngpus, int rank,
+                                int device, uint32_t flags) {
+  if (!out) return fail(EFFT_ERR_INVALID_ARG, "plan pointer is NULL");
+  *out = nullptr;
+  if (dtype != EFFT_C64 && dtype != EFFT_C128) return fail(EFFT_ERR_INVALID_ARG, "dtype %d (complex only)", dtype);
+  if (direction != EFFT_FORWARD && direction != EFFT_INVERSE)
+    return fail(EFFT_ERR_INVALID_ARG, "direction must be -1 or +1, got %d", direction);
+  if (ngpus < 2 || ngpus > 64 || (ngpus & (ngpus - 1)) || rank < 0 || rank >= ngpus)
+    return fail(EFFT_ERR_INVALID_ARG, "ngpus must be a power of two in [2, 64], 0 <= rank < ngpus");
+  const int c128 = dtype == EFFT_C128;
+  int64_t N1, N2;
+  if (!efft::lean::split_sharded(n, ngpus, c128, &N1, &N2))
+    return fail(EFFT_ERR_UNSUPPORTED_SIZE, "n=%lld cannot be sharded over %d ranks", (long long)n, ngpus);
+  int ndev = 0;
+  CUDA_TRY(cudaGetDeviceCount(&ndev));
+  if (device < 0 || device >= ndev) return fail(EFFT_ERR_INVALID_ARG, "device %d of %d", device, ndev);
+  CUDA_TRY(cudaSetDevice(device));
+  efft_plan_s* pl = new efft_plan_s();
+  pl->n = pl->n_user = n;
+  pl->dtype = dtype;
+  pl->direction = direction;
+  pl->device = device;
+  pl->flags = flags;
+  pl->elem = c128 ? 16 : 8;
+  pl->npass = 2;
+  pl->sh_n1 = N1;
+  pl->sh_n2 = N2;
+  pl->sh_rank = rank;
+  pl->sh_world = ngpus;
+  pl->ranks.resize(1);
+  auto& r = pl->ranks[0];
+  r.dev = device;
+  int sms = 0, ecuda = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+  int64_t stg = 0;
+  if (!efft::lean::plan_sharded(n, ngpus, rank, c128, direction == EFFT_INVERSE, (flags & EFFT_FLAG_CHECK_FINITE) != 0,
+                                sms, r.lp, &stg, &ecuda, true)) {
+    efft_plan_destroy(pl);
+    return ecuda ? fail(EFFT_ERR_CUDA, "shard pass setup failed") : fail(EFFT_ERR_UNSUPPORTED_SIZE, "no pass kernel");
+  }
+  r.counter_bytes = (size_t)(r.lp[0].counter_ints + r.lp[1].counter_ints) * 4;
+  if (cudaMalloc(&r.staging, (size_t)stg * pl->elem) != cudaSuccess ||
+      cudaMalloc((void**)&r.counters, r.counter_bytes) != cudaSuccess || cudaMalloc((void**)&r.flag, 4) != cudaSuccess ||
+      cudaMemset(r.flag, 0, 4) != cudaSuccess) {
+    cudaGetLastError();
+    efft_plan_destroy(pl);
+    return fail(EFFT_ERR_ALLOC, "shard rank buffers");
+  }
+  int64_t off = 0;
+  for (auto& ps : r.lp) {
+    ps.a.stg = r.staging;
+    ps.a.ctr = reinterpret_cast<unsigned long long*>(r.counters + off);
+    ps.a.doneA = r.counters + off + 2;
+    ps.a.doneB = ps.a.doneA + ps.a.ngroups;
+    ps.a.flag = r.flag;
+    off += ps.counter_ints;
+  }
+  *out = pl;
+  return EFFT_OK;
+}
+
+int efft_execute_shard_pass(efft_plan_t pl, int pass, const void* in, void* out, void* stream) {
+  if (!pl || !in || !out || pl->ranks.size() != 1 || pl->sh_world < 2)
+    return fail(EFFT_ERR_INVALID_ARG, "not a shard-rank plan or NULL buffer");
+  if (pass != 0 && pass != 1) return fail(EFFT_ERR_INVALID_ARG, "pass must be 0 or 1");
+  if (pass == 0 && in == out) return fail(EFFT_ERR_INVALID_ARG, "pass 0 cannot run in place");
+  auto& r = pl->ranks[0];
+  CUDA_TRY(cudaSetDevice(r.dev));
+  cudaStream_t s = (cudaStream_t)stream;
+  efft::lean::Pass& q = r.lp[pass];
+  CUDA_TRY(cudaMemsetAsync(q.a.ctr, 0, (size_t)q.counter_ints * 4, s));
+  return launch_lean(q, in, out, s);
+}
+
+int efft_sharded_split(efft_plan_t pl, int64_t* n1, int64_t* n2) {
+  if (!pl || !n1 || !n2 || pl->ranks.empty()) return fail(EFFT_ERR_INVALID_ARG, "not a sharded plan");
+  *n1 = pl->sh_n1;
+  *n2 = pl->sh_n2;
+  return EFFT_OK;
+}
+
 int efft_plan_destroy(efft_plan_t pl) {
   if (!pl) return EFFT_OK;
+  for (auto& r : pl->ranks) {
+    cudaSetDevice(r.dev);
+    if (r.staging) cudaFree(r.staging);
+    if (r.counters) cudaFree(r.counters);
+    if (r.flag) cudaFree(r.flag);
+    if (r.work) cudaFree(r.work);
+    if (r.ev) cudaEventDestroy(r.ev);
+  }
   cudaSetDevice(pl->device);
   for (auto& e : pl->tev)
     if (e) cudaEventDestroy(e);

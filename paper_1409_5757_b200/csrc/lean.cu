@@ -44,6 +44,7 @@
 // claims run two tasks ahead, the next task's producers are probed with
 // relaxed loads, and ONE fence.acq_rel per tile, issued right after the tile
 // loads, releases the previous tile and completes those acquires.
+#include <algorithm>
 #include <cstdlib>
 
 #include "efft_kernels.cuh"
@@ -89,6 +90,16 @@ __device__ __forceinline__ float2 cscale(float2 v, float2 c) { return mul2(v, c)
 __device__ __forceinline__ double2 cscale(double2 v, double2 c) { return make_double2(v.x * c.x, v.y * c.y); }
 __device__ __forceinline__ float2 cvt(double2 c, float) { return make_float2((float)c.x, (float)c.y); }
 __device__ __forceinline__ double2 cvt(double2 c, double) { return c; }
+
+// Pass-1 output offset of (local column j2, k1): the transposed layout
+// y[k1 + R j2], or, for the sharded transform's NCCL path (a.obl = log2 L1 >
+// 0), blocked by destination rank: [k1 / L1][j2][k1 % L1] (the all-to-all
+// send buffer, no pack pass).  k1 and k1 + 1 always share a block.
+__device__ __forceinline__ int64_t t1_out(const Args& a, int j2, uint32_t k1) {
+  if (a.obl == 0) return (int64_t)j2 * a.R + k1;
+  const uint32_t bl = 1u << a.obl;
+  return ((int64_t)(k1 >> a.obl) * a.LS + j2) * bl + (k1 & (bl - 1));
+}
 
 // Position -> (sub-stage, group, task) of the claim order above (thread 0 only).
 __device__ __forceinline__ void decode(const Args& a, uint32_t pos, int& isB, int& g, int& task) {
@@ -396,12 +407,12 @@ __global__ void __launch_bounds__(LT<R>::NT, MINB) lean_pass(const __grid_consta
         const uint32_t c = (uint32_t)(h * F + lane + 16 * ks + RA * kq);
         // W_N^(j2 k1) from the exact integer exponent: fp64 base and step
         // (sincospi), fp64 recurrence, one rounding per use (north star c)
-        double2 w = wroot((int64_t)(((uint64_t)j2 * c) % (uint64_t)a.N), a.N);
-        const double2 st = wroot((int64_t)(((uint64_t)j2 * (RA * QB)) % (uint64_t)a.N), a.N);
-        V* op = DST + (int64_t)j2 * a.R + c;
+        const uint64_t jg = (uint64_t)(a.j2off + j2);  // global column (sharded: rank offset)
+        double2 w = wroot((int64_t)((jg * c) % (uint64_t)a.N), a.N);
+        const double2 st = wroot((int64_t)((jg * (RA * QB)) % (uint64_t)a.N), a.N);
 #pragma unroll
         for (int kp = 0; kp < 16; ++kp) {
-          st_hint(op + kp * (RA * QB), cmul(v[P<16>(kp)], to_v(w, R())), pol);
+          st_hint(DST + t1_out(a, j2, c + kp * (RA * QB)), cmul(v[P<16>(kp)], to_v(w, R())), pol);
           if (kp < 15) w = cmul(w, st);
         }
       } else {
@@ -640,15 +651,15 @@ __global__ void __launch_bounds__(pair::NT, 4) lean_pair(const __grid_constant__
         // fp64 bases and step (sincospi), fp64 recurrence, one rounding per
         // use -- fp64-accurate twiddles on the fp32 path, no table (north star c)
         // (column kt + 1: times W_N^j2 in fp32, <= 1.5 ulp)
-        const uint64_t N = (uint64_t)a.N;
-        double2 w0 = wroot((int64_t)(((uint64_t)j2 * c) % N), a.N);
-        const V wj = to_v(wroot((int64_t)((uint64_t)j2 % N), a.N), 0.f);
-        const double2 st = wroot((int64_t)(((uint64_t)j2 * (256 * QB)) % N), a.N);
-        V* op = DST + (int64_t)j2 * a.R + c;
+        const uint64_t N = (uint64_t)a.N, jg = (uint64_t)(a.j2off + j2);  // global column
+        double2 w0 = wroot((int64_t)((jg * c) % N), a.N);
+        const V wj = to_v(wroot((int64_t)(jg % N), a.N), 0.f);
+        const double2 st = wroot((int64_t)((jg * (256 * QB)) % N), a.N);
 #pragma unroll
         for (int kp = 0; kp < 16; ++kp) {
           const V w = to_v(w0, 0.f);
-          pair::st16(op + kp * (256 * QB), cmul(x[P<16>(kp)], w), cmul(y[P<16>(kp)], cmul(w, wj)), pol);
+          pair::st16(DST + t1_out(a, j2, c + kp * (256 * QB)), cmul(x[P<16>(kp)], w), cmul(y[P<16>(kp)], cmul(w, wj)),
+                     pol);
           if (kp < 15) w0 = cmul(w0, st);
         }
       } else {
@@ -740,88 +751,142 @@ static bool use_pair() {
   return v != 0;
 }
 
+// One pass: column DFTs of length R = ra * rb over `cols` columns (row
+// stride cols), t1 = the transposing pass with the four-step twiddle
+// W_N^((j2off + j2) k1).  Returns false when no kernel covers it.
+static bool plan_pass(Pass& q, bool t1, int ra, int lb, int64_t cols, int64_t N, int64_t j2off, int c128,
+                      int inverse, bool scale_inverse, bool check_finite, int num_sms, int* err_cuda) {
+  const int F = c128 ? 8 : 16, NT = 16 * F;
+  const size_t elem = c128 ? 16 : 8;
+  if (cols < F || cols % F) return false;
+  q.ra = ra;
+  q.rb = 1 << lb;
+  const int64_t R = (int64_t)ra << lb;
+  const bool paired = !c128 && q.ra == 256 && use_pair();
+  q.fn = reinterpret_cast<void (*)(Args)>(paired ? pick_pair(q.rb, t1)
+                                          : c128 ? pick<double>(q.ra, q.rb, t1) : pick<float>(q.ra, q.rb, t1));
+  if (!q.fn) return false;
+  q.nt = paired ? pair::NT : NT;
+  // exchange (padded only in the transposing pass) + W_256 + W_R^(i<256) (+ two 192-entry tables)
+  q.smem = paired ? (int)(((t1 ? pair::XB2 : 4096) + 512) * elem)
+                  : (int)(((t1 ? 256 * (F + 1) : 256 * F) + 512 + (q.ra == 256 ? 0 : 2 * q.ra)) * elem);
+  Args& a = q.a;
+  a = Args{};
+  a.R = R;
+  a.N = N;
+  a.j2off = j2off;
+  a.LS = cols;
+  a.ngroups = (int32_t)(cols / F);
+  a.ntA = q.rb;
+  a.ntB = q.ra * q.rb / 256;
+  a.slot_elems = (int64_t)F * R;
+  a.total = (int64_t)a.ngroups * (a.ntA + a.ntB);
+  a.cin = make_double2(1.0, t1 && inverse ? -1.0 : 1.0);
+  const double sc = (!t1 && inverse && scale_inverse) ? 1.0 / (double)N : 1.0;
+  a.cout = make_double2(sc, (!t1 && inverse) ? -sc : sc);
+  a.check_finite = t1 && check_finite;
+  if (cudaFuncSetAttribute((const void*)q.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, q.smem) != cudaSuccess) {
+    *err_cuda = 1;
+    return false;
+  }
+  int occ = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void*)q.fn, q.nt, q.smem) != cudaSuccess ||
+      occ < 1) {
+    *err_cuda = 1;
+    return false;
+  }
+  q.grid = occ * num_sms;
+  // Claimed tasks in flight span about 3 grids: B(g) is issued `lag` groups
+  // after A(g), and A(g) reuses the slot of group g - nslots.
+  const int64_t per = (int64_t)a.ntA + a.ntB;
+  const int64_t window = (4 * (int64_t)q.grid + per - 1) / per;
+  int64_t lag = window + 1;
+  if (const char* ev = getenv("EFFT_LEAN_LAG")) lag = atoi(ev);
+  int64_t slots = lag + (window + 1) / 2 + 2;
+  if (const char* ev = getenv("EFFT_LEAN_SLOTS")) slots = atoi(ev);
+  if (lag < 1) lag = 1;
+  if (lag > a.ngroups) lag = a.ngroups;
+  if (slots < lag + 1) slots = lag + 1;
+  if (slots > a.ngroups) slots = a.ngroups;
+  a.lag = (int32_t)lag;
+  a.nslots = (int32_t)slots;
+  q.counter_ints = 2 + 2 * (int64_t)a.ngroups;
+  return true;
+}
+
+static bool factor_m(int64_t n, int& m, int& t) {
+  if (n <= 0) return false;
+  int64_t mm = n;
+  t = 0;
+  while ((mm & 1) == 0) {
+    mm >>= 1;
+    ++t;
+  }
+  m = (int)mm;
+  return m == 1 || m == 3 || m == 5 || m == 7;
+}
+
+// in-place pass: RA2 = 256, or 12 x 16 = 3 * 64, 10 x 16 = 5 * 32, 14 x 16 = 7 * 32
+static int ra_of(int m) { return m == 3 ? 192 : m == 5 ? 160 : m == 7 ? 224 : 256; }
+// log2(RB) of an R = ra * 2^lb pass; rho_b >= 32 (QB >= 2) in general, the
+// paired complex64 kernel also runs rho_b = 16 (QB = 1)
+static bool rb_ok(int lb, int c128, int m) { return lb >= ((!c128 && m == 1) ? 4 : 5) && lb <= 8; }
+
 bool plan(int64_t n, int c128, int inverse, bool scale_inverse, bool check_finite, int num_sms, Pass p[2],
           int64_t* staging_elems, int* err_cuda) {
   *err_cuda = 0;
-  if (n <= 0) return false;
-  int64_t m = n;
-  int t = 0;
-  while ((m & 1) == 0) {
-    m >>= 1;
-    ++t;
-  }
-  if (m != 1 && m != 3 && m != 5 && m != 7) return false;
-  // RA = 256, except RA = 192 in pass 2 (the in-place pass) when 3 | n;
-  // log2(RB1 RB2) = t - 16 (or t - 14)
-  // in-place pass: RA2 = 256, or 12 x 16 = 3 * 64, 10 x 16 = 5 * 32, 14 x 16 = 7 * 32
-  const int ra2 = m == 3 ? 192 : m == 5 ? 160 : m == 7 ? 224 : 256;
+  int m, t;
+  if (!factor_m(n, m, t)) return false;
+  // RA = 256, except RA = 192 / 160 / 224 in pass 2 (the in-place pass) when 3 / 5 / 7 | n
+  const int ra2 = ra_of(m);
   const int lbs = m == 1 ? t - 16 : m == 3 ? t - 14 : t - 13;
   const int lb1 = (lbs + 1) / 2, lb2 = lbs - lb1;
-  // rho_b >= 32 (QB >= 2) in general; the paired complex64 kernel also runs
-  // rho_b = 16 (QB = 1: the B stage is one 16-point DFT), down to N = 2^24
-  const int lbmin = (!c128 && m == 1) ? 4 : 5;
-  if (lb1 < lbmin || lb1 > 8 || lb2 < lbmin || lb2 > 8) return false;
+  if (!rb_ok(lb1, c128, m) || !rb_ok(lb2, c128, m)) return false;
   const int64_t R1 = int64_t(256) << lb1, R2 = (int64_t)ra2 << lb2;
-  const int F = c128 ? 8 : 16, NT = 16 * F;
-  const size_t elem = c128 ? 16 : 8;
-  int64_t stg = 0;
-  for (int i = 0; i < 2; ++i) {
-    Pass& q = p[i];
-    const bool t1 = i == 0;
-    const int64_t R = t1 ? R1 : R2;
-    q.ra = t1 ? 256 : ra2;
-    q.rb = 1 << (t1 ? lb1 : lb2);
-    const bool paired = !c128 && q.ra == 256 && use_pair();
-    q.fn = reinterpret_cast<void (*)(Args)>(paired ? pick_pair(q.rb, t1)
-                                            : c128 ? pick<double>(q.ra, q.rb, t1) : pick<float>(q.ra, q.rb, t1));
-    if (!q.fn) return false;
-    q.nt = paired ? pair::NT : NT;
-    // exchange (padded only in the transposing pass) + W_256 + W_R^(i<256) (+ two 192-entry tables)
-    q.smem = paired ? (int)(((t1 ? pair::XB2 : 4096) + 512) * elem)
-                    : (int)(((t1 ? 256 * (F + 1) : 256 * F) + 512 + (q.ra == 256 ? 0 : 2 * q.ra)) * elem);
-    Args& a = q.a;
-    a = Args{};
-    a.R = R;
-    a.N = n;
-    a.LS = t1 ? R2 : R1;
-    a.ngroups = (int32_t)((t1 ? R2 : R1) / F);
-    a.ntA = q.rb;
-    a.ntB = q.ra * q.rb / 256;
-    a.slot_elems = (int64_t)F * R;
-    a.total = (int64_t)a.ngroups * (a.ntA + a.ntB);
-    a.cin = make_double2(1.0, t1 && inverse ? -1.0 : 1.0);
-    const double sc = (!t1 && inverse && scale_inverse) ? 1.0 / (double)n : 1.0;
-    a.cout = make_double2(sc, (!t1 && inverse) ? -sc : sc);
-    a.check_finite = t1 && check_finite;
-    if (cudaFuncSetAttribute((const void*)q.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, q.smem) != cudaSuccess) {
-      *err_cuda = 1;
-      return false;
-    }
-    int occ = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void*)q.fn, q.nt, q.smem) != cudaSuccess ||
-        occ < 1) {
-      *err_cuda = 1;
-      return false;
-    }
-    q.grid = occ * num_sms;
-    // Claimed tasks in flight span about 3 grids: B(g) is issued `lag` groups
-    // after A(g), and A(g) reuses the slot of group g - nslots.
-    const int64_t per = (int64_t)a.ntA + a.ntB;
-    const int64_t window = (4 * (int64_t)q.grid + per - 1) / per;
-    int64_t lag = window + 1;
-    if (const char* ev = getenv("EFFT_LEAN_LAG")) lag = atoi(ev);
-    int64_t slots = lag + (window + 1) / 2 + 2;
-    if (const char* ev = getenv("EFFT_LEAN_SLOTS")) slots = atoi(ev);
-    if (lag < 1) lag = 1;
-    if (lag > a.ngroups) lag = a.ngroups;
-    if (slots < lag + 1) slots = lag + 1;
-    if (slots > a.ngroups) slots = a.ngroups;
-    a.lag = (int32_t)lag;
-    a.nslots = (int32_t)slots;
-    q.counter_ints = 2 + 2 * (int64_t)a.ngroups;
-    if (slots * a.slot_elems > stg) stg = slots * a.slot_elems;
+  if (!plan_pass(p[0], true, 256, lb1, R2, n, 0, c128, inverse, scale_inverse, check_finite, num_sms, err_cuda) ||
+      !plan_pass(p[1], false, ra2, lb2, R1, n, 0, c128, inverse, scale_inverse, check_finite, num_sms, err_cuda))
+    return false;
+  *staging_elems = std::max(p[0].a.nslots * p[0].a.slot_elems, p[1].a.nslots * p[1].a.slot_elems);
+  return true;
+}
+
+bool split_sharded(int64_t n, int G, int c128, int64_t* N1, int64_t* N2) {
+  int m, t;
+  if (!factor_m(n, m, t) || G < 1 || (G & (G - 1))) return false;
+  const int ra2 = ra_of(m);
+  const int lbs = m == 1 ? t - 16 : m == 3 ? t - 14 : t - 13;
+  const int lb1 = (lbs + 1) / 2, lb2 = lbs - lb1;
+  if (!rb_ok(lb1, c128, m) || !rb_ok(lb2, c128, m)) return false;
+  *N1 = int64_t(256) << lb1;
+  *N2 = (int64_t)ra2 << lb2;
+  const int F = c128 ? 8 : 16;
+  return *N1 % ((int64_t)G * F) == 0 && *N2 % ((int64_t)G * F) == 0;
+}
+
+bool plan_sharded(int64_t n, int G, int rank, int c128, int inverse, bool check_finite, int num_sms, Pass p[2],
+                  int64_t* staging_elems, int* err_cuda, bool blocked) {
+  *err_cuda = 0;
+  int64_t N1, N2;
+  if (!split_sharded(n, G, c128, &N1, &N2)) return false;
+  int m, t;
+  factor_m(n, m, t);
+  const int ra2 = ra_of(m);
+  int lb1 = 0, lb2 = 0;
+  while ((int64_t(256) << lb1) < N1) ++lb1;
+  while (((int64_t)ra2 << lb2) < N2) ++lb2;
+  const int64_t L1 = N1 / G, L2 = N2 / G;
+  // pass 1 over this rank's L2 columns (global columns rank * L2 + c), pass 2 over its L1 columns
+  if (!plan_pass(p[0], true, 256, lb1, L2, n, (int64_t)rank * L2, c128, inverse, true, check_finite, num_sms,
+                 err_cuda) ||
+      !plan_pass(p[1], false, ra2, lb2, L1, n, 0, c128, inverse, true, check_finite, num_sms, err_cuda))
+    return false;
+  if (blocked) {
+    int lg = 0;
+    while ((int64_t(1) << lg) < L1) ++lg;
+    if ((int64_t(1) << lg) != L1 || L1 < 2) return false;
+    p[0].a.obl = lg;
   }
-  *staging_elems = stg;
+  *staging_elems = std::max(p[0].a.nslots * p[0].a.slot_elems, p[1].a.nslots * p[1].a.slot_elems);
   return true;
 }
 

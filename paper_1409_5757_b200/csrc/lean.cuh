@@ -27,6 +27,9 @@ struct Args {
   int64_t LS;          // element stride between successive DFT points in src
   int64_t R;           // DFT length of the pass (256 * RB)
   int64_t N;           // full transform length (four-step twiddle of pass 1)
+  int64_t j2off;       // pass 1: global index of the first column (sharded ranks; 0 otherwise)
+  int32_t obl;         // pass 1: 0 = transposed output y[k1 + R j2]; else log2 L1 of the blocked
+                       //   layout [k1 / L1][j2][k1 % L1] (sharded NCCL path)
   int64_t slot_elems;  // F * R: one column group
   int64_t total;       // ngroups * (ntA + ntB) tasks
   int32_t ngroups, nslots, lag;
@@ -52,6 +55,15 @@ struct Pass {
 // (err_cuda set when a CUDA call failed).  Reports the staging elements needed.
 bool plan(int64_t n, int c128, int inverse, bool scale_inverse, bool check_finite, int num_sms, Pass p[2],
           int64_t* staging_elems, int* err_cuda);
+
+// Six-step over G ranks (efft_execute_sharded): N = N1 N2, G | N1 / F and
+// G | N2 / F.  Rank q's local steps are the same two passes on its blocks:
+//   pass 1: B_q[n1][c] (N1 x L2, global column q L2 + c) -> Y'_q[c][k1] with
+//           W_N^((q L2 + c) k1) fused into the transposing store;
+//   pass 2: T_q[n2][k1'] (N2 x L1) -> X_q[k2][k1'] in place (inverse: 1/N).
+bool split_sharded(int64_t n, int G, int c128, int64_t* N1, int64_t* N2);
+bool plan_sharded(int64_t n, int G, int rank, int c128, int inverse, bool check_finite, int num_sms, Pass p[2],
+                  int64_t* staging_elems, int* err_cuda, bool blocked = false);
 
 }  // namespace lean
 }  // namespace efft

@@ -1,9 +1,11 @@
-"""Sharded six-step on ONE B200: G emulated ranks as host threads, each with its
-own CUDA stream; the all-to-all is a host-barrier-synchronised copy between
-the ranks' device buffers (no kernel ever waits on another kernel).  Exercises
-the product's local steps -- column plans (staged/direct passes) and the
-permutation kernels -- for G = 2, 4, 8; the NCCL exchange itself is covered by
-tests/test_sharded.py over gloo."""
+"""Sharded six-step (one process per GPU path, sharded.py) on ONE B200: G
+emulated ranks as host threads, each with its own CUDA stream; the all-to-all
+is a host-barrier-synchronised copy between the ranks' device buffers (no
+kernel ever waits on another kernel).  Exercises the product's local steps --
+the shard-rank lean passes (efft_plan_create_shard_rank: pass 0 with the
+blocked transposing store, pass 1 in place) and the pack / unpack kernels --
+for G = 2, 4, 8; the NCCL exchange itself is covered by tests/test_sharded.py
+over gloo and by test_nccl_two_gpus below when two GPUs are present."""
 import threading
 
 import numpy as np
@@ -80,8 +82,8 @@ def run_emulated(x, world, dtype, direction):
 
 
 @pytest.mark.parametrize("world", [2, 4, 8])
-@pytest.mark.parametrize("dtype", ["complex64", "complex128"])
-@pytest.mark.parametrize("n", [1 << 20, 3 << 20, 1 << 24])
+@pytest.mark.parametrize("dtype,n", [("complex64", 1 << 24), ("complex64", 3 << 24), ("complex128", 1 << 26),
+                                     ("complex128", 3 << 24)])
 def test_sharded_emulated_matches_oracle(world, dtype, n):
     rng = np.random.default_rng(world + n)
     x = rng.standard_normal(n) + 1j * rng.standard_normal(n)
@@ -91,3 +93,51 @@ def test_sharded_emulated_matches_oracle(world, dtype, n):
     assert oracle.rel_l2(y, oracle.transform(x)) <= tol
     z = run_emulated(y, world, dtype, 1)
     assert oracle.rel_l2(z, x) <= 2 * tol
+
+
+def _nccl_worker(rank, world, port, n, q):
+    import os
+
+    import torch.distributed as dist
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(rank)
+    dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", rank))
+    try:
+        rng = np.random.default_rng(11)
+        x = rng.standard_normal(n) + 1j * rng.standard_normal(n)
+        shard = n // world
+        xl = torch.from_numpy(x[rank * shard:(rank + 1) * shard].astype(np.complex64)).cuda()
+        yl, w = torch.empty_like(xl), torch.empty_like(xl)
+        t = sharded.ShardedTransform(n, world, rank, -1, sharded.GpuBackend("complex64", rank))
+        t.execute(xl, yl, w)
+        torch.cuda.synchronize()
+        q.put((rank, yl.cpu().numpy()))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_nccl_two_gpus():
+    """The NCCL data plane on 2 real GPUs against the oracle (skipped on 1-GPU boxes)."""
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs 2 GPUs")
+    import socket
+
+    import torch.multiprocessing as mp
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    n, world = 1 << 24, 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    ps = [ctx.Process(target=_nccl_worker, args=(r, world, port, n, q)) for r in range(world)]
+    for p in ps:
+        p.start()
+    parts = dict(q.get(timeout=300) for _ in range(world))
+    for p in ps:
+        p.join(timeout=60)
+    y = np.concatenate([parts[r] for r in range(world)])
+    rng = np.random.default_rng(11)
+    x = rng.standard_normal(n) + 1j * rng.standard_normal(n)
+    assert oracle.rel_l2(y, oracle.transform(x)) <= 1e-5 * 24

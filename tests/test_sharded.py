@@ -15,28 +15,37 @@ from paper_1409_5757_b200 import sharded
 
 
 class CpuBackend:
-    """Test stand-in for GpuBackend: numpy permutations, oracle pass, gloo all-to-all."""
+    """Test stand-in for GpuBackend: numpy passes with the same contract as the
+    shard-rank plan (efft_execute_shard_pass), numpy permutations, gloo all-to-all."""
 
-    def column_plan(self, length, cols, direction, tw_mod, tw_offset, scale):
-        return dict(length=length, cols=cols, direction=direction, tw_mod=tw_mod, tw_offset=tw_offset,
-                    scale=scale)
+    def split(self, n, world):
+        # any N1 x N2 works for the numpy passes; small test sizes use a balanced split
+        m, t = sharded._factor(n)
+        t1 = t // 2
+        return m << t1, 1 << (t - t1)
 
-    def run(self, plan, src, dst):
-        a = src.numpy().copy()
-        out = np.empty_like(a)
-        oracle.pass_c128(a, out, length=plan["length"], cols=plan["cols"], batch=1, in_col=1,
-                         in_stride=plan["cols"], in_batch=0, out_col=1, out_stride=plan["cols"],
-                         out_batch=0, tw_mod=plan["tw_mod"], tw_base=plan["tw_offset"], tw_col=1,
-                         direction=plan["direction"], threads=1)
-        if plan["scale"]:
-            out /= plan["length"]
-        dst.numpy()[:] = out
+    def shard_plan(self, n, world, rank, direction, n1, n2):
+        return dict(n=n, world=world, rank=rank, direction=direction, n1=n1, n2=n2)
+
+    def pass0(self, plan, src, dst):
+        n, G, p, d, n1, n2 = (plan[k] for k in ("n", "world", "rank", "direction", "n1", "n2"))
+        l1, l2 = n1 // G, n2 // G
+        b = src.numpy().reshape(n1, l2)
+        y = np.fft.fft(b, axis=0) if d == -1 else np.fft.ifft(b, axis=0) * n1
+        k1 = np.arange(n1)[:, None]
+        c = (p * l2 + np.arange(l2))[None, :]
+        y = y * np.exp(d * 2j * np.pi * ((c * k1) % n) / n)  # W_N^(n2 k1)
+        # blocked by destination rank: [q][c][k1']
+        dst.numpy()[:] = y.reshape(G, l1, l2).transpose(0, 2, 1).reshape(-1)
+
+    def pass1(self, plan, buf):
+        n, G, d, n1, n2 = (plan[k] for k in ("n", "world", "direction", "n1", "n2"))
+        t = buf.numpy().reshape(n2, n1 // G)
+        x = np.fft.fft(t, axis=0) if d == -1 else np.fft.ifft(t, axis=0) / n1
+        buf.numpy()[:] = x.reshape(-1)
 
     def swap01(self, src, dst, n0, n1, n2):
         dst.numpy()[:] = src.numpy().reshape(n0, n1, n2).transpose(1, 0, 2).reshape(-1)
-
-    def swap12(self, src, dst, n0, n1, n2):
-        dst.numpy()[:] = src.numpy().reshape(n0, n1, n2).transpose(0, 2, 1).reshape(-1)
 
     def all_to_all(self, src, dst):
         # gloo has no complex all_to_all: exchange the float64 view
@@ -92,16 +101,18 @@ def test_sharded_matches_oracle(world, n, direction):
 
 
 def test_split_sizes():
+    """the Python mirror of lean.cu split_sharded (the GPU test checks the two agree)"""
     assert sharded.split_sizes(1 << 30, 8) == (1 << 15, 1 << 15)
-    assert sharded.split_sizes(3 << 28, 8) == (3 << 14, 1 << 14)
-    n1, n2 = sharded.split_sizes(1 << 32, 4)
-    assert n1 * n2 == 1 << 32 and n1 % 4 == 0 and n2 % 4 == 0
-    assert sharded.split_sizes(5 << 20, 2) == (5 << 10, 1 << 10)
-    assert sharded.split_sizes(7 << 20, 2) == (7 << 10, 1 << 10)
+    assert sharded.split_sizes(1 << 32, 8, "complex128") == (1 << 16, 1 << 16)
+    assert sharded.split_sizes(3 << 28, 8, "complex128") == (1 << 15, 3 << 13)
+    assert sharded.split_sizes(1 << 27, 4, "complex128") == (1 << 14, 1 << 13)
+    assert sharded.split_sizes(5 << 24, 2) == (1 << 14, 5 << 10)
     with pytest.raises(ValueError):
         sharded.split_sizes(9 << 20, 2)
     with pytest.raises(ValueError):
-        sharded.split_sizes(1 << 20, 3)
+        sharded.split_sizes(1 << 30, 3)
+    with pytest.raises(ValueError):
+        sharded.split_sizes(1 << 20, 2)  # below the pass range
 
 
 def test_exchange_bytes_model():
