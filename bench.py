@@ -42,8 +42,33 @@ import time
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-DTYPE_NAME = {"complex64": "f32", "complex128": "f64"}
-ELEM = {"complex64": 8, "complex128": 16}
+DTYPE_NAME = {"complex64": "f32", "complex128": "f64", "float32": "f32"}
+# complex input: BASELINE.json's 5 N log2 N; real input: the reference's own 2.5 N log2 N
+METRIC = {False: "GFLOP/s (5N*log2N) per 1D FFT", True: "GFLOP/s (2.5N*log2N, real input) per 1D FFT"}
+ELEM = {"complex64": 8, "complex128": 16, "float32": 4}
+
+
+def flops_of(cfg):
+    """5 N log2 N for complex input (BASELINE.json), 2.5 N log2 N for real input
+    (the reference's own model, bench.py:27-31)."""
+    n = cfg["n"]
+    return (2.5 if cfg["dtype"] == "float32" else 5.0) * n * math.log2(n)
+
+
+def pass_alg_bytes(cfg):
+    """One read + one write of the array a pass kernel transforms (real input:
+    the N/2-point complex64 transform)."""
+    n = cfg["n"]
+    return 2 * (n // 2) * 8 if cfg["dtype"] == "float32" else 2 * n * ELEM[cfg["dtype"]]
+
+
+def as_oracle_complex(x_np, cfg):
+    """The complex array the oracle transforms: real input as complex."""
+    import numpy as np
+
+    if cfg["dtype"] == "float32":
+        return x_np.astype(np.complex128)
+    return x_np
 
 
 def measured_peaks():
@@ -151,7 +176,9 @@ def cpu_baseline(cfg_name, cfg, x_dev, max_seconds=25.0):
     import oracle
 
     threads = oracle.host_threads()
-    prec = "c64" if cfg["dtype"] == "complex64" else "c128"
+    prec = "c128" if cfg["dtype"] == "complex128" else "c64"
+    if cfg["dtype"] == "float32":
+        return cpu_baseline_real(cfg_name, cfg, x_dev, threads, max_seconds)
     n_full = cfg["n"]
     # bounded sample: the largest power-of-two prefix (x 3 for C4) that runs in ~max_seconds
     m = 3 if n_full % 3 == 0 else 1
@@ -181,6 +208,36 @@ def cpu_baseline(cfg_name, cfg, x_dev, max_seconds=25.0):
                       f"({kind}) with {threads} OpenMP threads",
             "python_reference_context": PY_REFERENCE_CONTEXT}
     return line, (out if n == n_full else None), (host if n == n_full else None)
+
+
+def cpu_baseline_real(cfg_name, cfg, x_dev, threads, max_seconds):
+    """Real input: the oracle's float32 transform of the N/2-point complex
+    packing x[2j] + i x[2j+1] -- the core of the reference's real algorithm
+    (leaf_dft.py:93-125) -- on the largest prefix that runs in ~max_seconds."""
+    import numpy as np
+
+    import oracle
+
+    n_full = cfg["n"]
+    n = min(n_full, 1 << 22)
+    best = None
+    while True:
+        xr = x_dev[:n].cpu().numpy()
+        z = np.ascontiguousarray(xr[0::2] + 1j * xr[1::2]).astype(np.complex64)
+        t0 = time.perf_counter()
+        oracle.transform(z, precision="c64", threads=threads)
+        dt = time.perf_counter() - t0
+        best = (n, dt)
+        if n >= n_full or dt * 2.3 > max_seconds:
+            break
+        n *= 2
+    n, dt = best
+    return {"value": round(2.5 * n * math.log2(n) / dt / 1e9, 3), "unit": "GFLOP/s", "cores": threads,
+            "kind": "port",
+            "sample": f"the oracle's float32 c64 transform of the N/2 = {n // 2} point complex packing of a "
+                      f"{'whole' if n == n_full else 'prefix of the'} {cfg_name} real input ({dt:.2f} s, "
+                      f"2.5 N log2 N), oracle/efft_oracle.c with {threads} OpenMP threads",
+            "python_reference_context": PY_REFERENCE_CONTEXT}, None, None
 
 
 # The reference package itself (Python, real float32 two-real composition) is
@@ -217,6 +274,39 @@ def device_rel_l2(a, b, chunk=1 << 26):
     return math.sqrt(num / den)
 
 
+def parity_report_real(cfg, x, y):
+    """Real input (PERM output): relative L2 over the packed slots against the
+    fp64 restatement of the same input, the reference's own acceptance measure
+    and tolerance (test_acceptance.py:33-51: <= 1e-6; oracle.py:115-127)."""
+    import numpy as np
+
+    import oracle
+
+    n = cfg["n"]
+    out = {"tolerance": 1e-6, "comparator": "oracle fp64 restatement, packed as the reference's PERM layout"}
+    try:
+        import psutil
+
+        avail = psutil.virtual_memory().available
+    except Exception:
+        avail = 0
+    if avail < n * 48 + (8 << 30):
+        out["rel_l2"] = None
+        out["note"] = "host memory too small for the full-array comparator"
+        return out
+    xh = x.cpu().numpy()
+    f = oracle.transform(xh.astype(np.complex128))
+    packed = np.empty(n)
+    packed[0], packed[1] = f[0].real, f[n // 2].real
+    packed[2::2], packed[3::2] = f[1:n // 2].real, f[1:n // 2].imag
+    del f
+    yh = y.cpu().numpy().astype(np.float64)
+    err = float(np.linalg.norm(yh - packed) / np.linalg.norm(packed))
+    out["rel_l2"] = float(f"{err:.4e}")
+    out["within_tolerance"] = err <= 1e-6
+    return out
+
+
 def parity_report(cfg, x, y, inv_plan, oracle_out, x_host, sid):
     """Full-array parity of the timed transform's output y = F(x) (north star:
     rel-L2 <= 1e-5 log2N (c64) / 1e-12 log2N (c128) against the reference CPU
@@ -227,6 +317,8 @@ def parity_report(cfg, x, y, inv_plan, oracle_out, x_host, sid):
     import oracle
 
     n, dtype = cfg["n"], cfg["dtype"]
+    if dtype == "float32":
+        return parity_report_real(cfg, x, y)
     tol = (1e-5 if dtype == "complex64" else 1e-12) * math.log2(n)
     out = {"tolerance": tol}
     # forward -> inverse round trip on the device (the inverse plan scales by 1/N)
@@ -288,7 +380,8 @@ def run_reference(args):
     from paper_1409_5757_b200 import workloads
 
     cfg = workloads.CONFIGS[args.config]
-    prec = "c64" if cfg["dtype"] == "complex64" else "c128"
+    real = cfg["dtype"] == "float32"
+    prec = "c128" if cfg["dtype"] == "complex128" else "c64"
     threads = oracle.host_threads()
     n = cfg["n"]
     elem = 8 if prec == "c64" else 16
@@ -316,6 +409,8 @@ def run_reference(args):
         x = (rng.standard_normal(n) + 1j * rng.standard_normal(n)).astype(
             np.complex64 if prec == "c64" else np.complex128)
         gen = "numpy default_rng(seed) N(0,1) (no GPU visible: same distribution, different values)"
+    if real:  # the real transform's core: the N/2-point complex packing (leaf_dft.py:93-125)
+        x = np.ascontiguousarray(x[0::2] + 1j * x[1::2]).astype(np.complex64)
     out = np.empty_like(x)
     per_step = 2 if cfg["roundtrip"] else 1
     for _ in range(args.warmup):
@@ -326,11 +421,12 @@ def run_reference(args):
             oracle.transform(x if r == 0 else out, direction=-1 if r == 0 else 1, precision=prec,
                              threads=threads, out=out if r == 0 else x)
     dt = time.perf_counter() - t0
-    flops = 5.0 * n * math.log2(n) * per_step * args.steps
+    flops = (2.5 if real else 5.0) * n * math.log2(n) * per_step * args.steps
     gflops = flops / dt / 1e9
-    what = f"{per_step} {prec} transform(s) of N={n}" + ("" if same else f" (host RAM caps the full N={cfg['n']})")
+    what = (f"one c64 transform of the N/2 = {n // 2} point complex packing of the real input" if real else
+            f"{per_step} {prec} transform(s) of N={n}") + ("" if same else f" (host RAM caps the full N={cfg['n']})")
     line = {
-        "impl": "reference", "metric": "GFLOP/s (5N*log2N) per 1D FFT",
+        "impl": "reference", "metric": METRIC[real],
         "value": round(gflops, 3), "unit": "GFLOP/s", "n_gpus": args.gpus, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(dt / args.steps * 1e3, 3),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
@@ -400,7 +496,7 @@ def run_sharded(args, rank, local, world):
     t_roof = hbm_bytes / (peak * 1e9) + exch / 770e9
     if rank == 0:
         line = {
-            "metric": "GFLOP/s (5N*log2N) per 1D FFT",
+            "metric": METRIC[cfg["dtype"] == "float32"],
             "value": round(value, 3), "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps,
             "warmup": max(args.warmup, 3), "ms_per_step": round(ms_per_step, 4),
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
@@ -440,12 +536,13 @@ def run_ours(args):
     seed = workloads.seed_for(args.config) + rank
     x = workloads.make_input(n, dtype, cfg["kind"], seed, device="cuda")
     y = torch.empty_like(x)
-    ndt = _native.EFFT_C64 if dtype == "complex64" else _native.EFFT_C128
+    ndt = {"complex64": _native.EFFT_C64, "complex128": _native.EFFT_C128, "float32": _native.EFFT_R32}[dtype]
     # the flags the drop-in handle uses (core.TransformHandle): the non-finite
     # input check of the reference's scatter (scatter.py:38-39) is timed too
     flags = _native.EFFT_FLAG_CHECK_FINITE
     fwd = _native.NativePlan(n, ndt, -1, local, flags)
-    inv = _native.NativePlan(n, ndt, 1, local, flags | _native.EFFT_FLAG_SCALE_INVERSE)
+    # (real input has no inverse entry: the reference's PERM path is forward only)
+    inv = None if dtype == "float32" else _native.NativePlan(n, ndt, 1, local, flags | _native.EFFT_FLAG_SCALE_INVERSE)
     fwd.enable_timing(args.steps)  # per-launch events of every timed step (averaged)
     stream = torch.cuda.current_stream()
     sid = stream.cuda_stream
@@ -490,7 +587,7 @@ def run_ours(args):
     barrier(world)
     total_ms = max_over_ranks(total_ms, world)
     ms_per_step = total_ms / args.steps
-    flops_per_transform = 5.0 * n * math.log2(n)
+    flops_per_transform = flops_of(cfg)
     value = world * per_step * flops_per_transform * args.steps / (total_ms * 1e-3) / 1e9
 
     # dominant kernel roofline (pass kernels move 2*N*elem algorithmic bytes each)
@@ -498,7 +595,7 @@ def run_ours(args):
     # per-launch durations averaged over every timed step (events on the launching stream)
     avg = fwd.launch_times_ms()
     dom = max(range(len(avg)), key=lambda k: avg[k])
-    alg_bytes = 2 * n * ELEM[dtype]
+    alg_bytes = pass_alg_bytes(cfg)
     achieved = alg_bytes / (avg[dom] * 1e-3) / 1e9
     traffic = None  # DRAM bytes per launch of that kernel from the committed ncu capture
     try:
@@ -581,7 +678,7 @@ def run_ours(args):
 
     if rank == 0:
         line = {
-            "metric": "GFLOP/s (5N*log2N) per 1D FFT",
+            "metric": METRIC[cfg["dtype"] == "float32"],
             "value": round(value, 3), "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps,
             "warmup": max(args.warmup, 3), "ms_per_step": round(ms_per_step, 4),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
@@ -617,7 +714,7 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default="c3", choices=["c1", "c2", "c3", "c4", "c5"])
+    ap.add_argument("--config", default="c3", choices=["c1", "c2", "c3", "c4", "c5", "r24", "r27", "r30"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--no-e2e", action="store_true", help="skip the host-buffer e2e leg")

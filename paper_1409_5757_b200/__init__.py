@@ -24,6 +24,8 @@ from .core import (
     build_scatter_index,
     data_view,
     handle_create,
+    l2_norm,
+    pack_perm,
     plan_create,
     result_view,
     run_transform,
@@ -45,6 +47,8 @@ __all__ = [
     "outofcore",
     "flops_model",
     "handle_create",
+    "l2_norm",
+    "pack_perm",
     "plan_create",
     "result_view",
     "run_transform",

@@ -359,3 +359,38 @@ class PermSpectrum:
         out[: m // 2 + 1] = half
         out[m // 2 + 1:] = np.conj(half[-2:0:-1])
         return out
+
+
+def pack_perm(coeffs) -> np.ndarray:
+    """Coefficients F_0 .. F_{M/2} of a real length-M input -> the packed layout
+    [R_0, R_{M/2}, R_1, I_1, ..., R_{M/2-1}, I_{M/2-1}] (the reference's layout
+    contract, core.py:10-15 / oracle.py:92-112); F_0 and F_{M/2} must be real."""
+    from .errors import NotRealSpectrum
+
+    f = np.asarray(coeffs, dtype=np.complex128)
+    if f.ndim != 1 or f.shape[0] < 2:
+        raise ValueError("need the coefficients k = 0 .. M/2 of an M >= 2 point real transform")
+    m = 2 * (f.shape[0] - 1)
+    tol = 1e-9 * max(float(np.linalg.norm(f)), 1.0)
+    if abs(f[0].imag) > tol or abs(f[-1].imag) > tol:
+        raise NotRealSpectrum("DC and Nyquist terms must be real")
+    out = np.empty(m)
+    out[0], out[1] = f[0].real, f[-1].real
+    out[2::2], out[3::2] = f[1:-1].real, f[1:-1].imag
+    return out
+
+
+def l2_norm(computed, exact) -> float:
+    """Relative L2 deviation of `computed` from `exact` over packed slots, in fp64
+    (the reference's accuracy measure, oracle.py:115-127)."""
+    from .errors import ZeroReference
+
+    a = np.asarray(computed, dtype=np.float64)
+    b = np.asarray(exact, dtype=np.float64)
+    if a.shape != b.shape:
+        raise ValueError(f"length mismatch: {a.shape} vs {b.shape}")
+    den = float(np.linalg.norm(b))
+    if den == 0.0:
+        raise ZeroReference("the comparator has zero norm")
+    return float(np.linalg.norm(a - b)) / den
+

@@ -38,36 +38,42 @@ namespace {
 // half-length complex spectrum Z of the n/2 pairs):
 //   F_k = Z_k P_k + conj(Z_{h-k}) Q_k,  P_k = 1/2 - i/2 w^k,  Q_k = 1/2 + i/2 w^k,
 //   w = exp(-2 pi i / n); packed as [F_0, F_{n/2}, Re F_1, Im F_1, ...].
-// Thread k in [0, h/2] owns the pair (k, h-k) so the update is in place.
+// Each pair (k, h-k), 0 < k < h/2, is updated in place by one thread; thread t
+// of T handles k = 1 + t + j T, j < SPLIT_K, with w^k from one fp64 sincospi
+// base and an fp64 recurrence by w^T (w^(h-k) = -conj(w^k): no second angle).
+constexpr int SPLIT_K = 8;
 __global__ void real_split_kernel(float2* z, int64_t h, int64_t n) {
-  const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (k > h / 2) return;
-  if (k == 0) {
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t T = (int64_t)gridDim.x * blockDim.x;
+  if (t == 0) {
     const float2 z0 = z[0];
     z[0] = make_float2(z0.x + z0.y, z0.x - z0.y);
     if (h > 1 && (h & 1) == 0) {  // k = h/2 is self-paired: F = conj(Z)
       const float2 zm = z[h / 2];
       z[h / 2] = make_float2(zm.x, -zm.y);
     }
-    return;
   }
-  if (2 * k == h) return;  // handled by k == 0
-  const int64_t kk = h - k;
-  const float2 a = z[k], b = z[kk];
-  double s1, c1, s2, c2;
-  sincospi(-2.0 * (double)k / (double)n, &s1, &c1);
-  sincospi(-2.0 * (double)kk / (double)n, &s2, &c2);
-  // F_k with w^k = (c1, s1): P = (1/2 + s1/2, -c1/2), Q = (1/2 - s1/2, c1/2)
-  auto out = [](float2 zk, float2 zr, double c, double s) {
-    const double pr = 0.5 + 0.5 * s, pi = -0.5 * c, qr = 0.5 - 0.5 * s, qi = 0.5 * c;
+  int64_t k = 1 + t;
+  if (2 * k >= h) return;
+  double c, s, cs, ss;
+  sincospi(-2.0 * (double)k / (double)n, &s, &c);
+  sincospi(-2.0 * (double)T / (double)n, &ss, &cs);
+  // F for (zk, zr = Z_{h-k}) with w = (c, s): P = (1/2 + s/2, -c/2), Q = (1/2 - s/2, c/2)
+  auto out = [](float2 zk, float2 zr, double c_, double s_) {
+    const double pr = 0.5 + 0.5 * s_, pi = -0.5 * c_, qr = 0.5 - 0.5 * s_, qi = 0.5 * c_;
     const double cr = zr.x, ci = -zr.y;  // conj(Z_{h-k})
     return make_float2((float)(zk.x * pr - zk.y * pi + cr * qr - ci * qi),
                        (float)(zk.x * pi + zk.y * pr + cr * qi + ci * qr));
   };
-  const float2 fk = out(a, b, c1, s1);
-  const float2 fkk = out(b, a, c2, s2);
-  z[k] = fk;
-  z[kk] = fkk;
+  for (int j = 0; j < SPLIT_K && 2 * k < h; ++j, k += T) {
+    const int64_t kk = h - k;
+    const float2 a = z[k], b = z[kk];
+    z[k] = out(a, b, c, s);
+    z[kk] = out(b, a, -c, s);  // w^(h-k) = -conj(w^k)
+    const double cn = c * cs - s * ss;
+    s = c * ss + s * cs;
+    c = cn;
+  }
 }
 
 thread_local std::string g_err;
@@ -884,8 +890,9 @@ int efft_execute(efft_plan_t pl, const void* d_in, void* d_out, void* stream) {
   }
   if (ev) CUDA_TRY(cudaEventRecord(ev[pl->npass], s));
   if (pl->real_input) {
-    const int64_t h = pl->n, work = h / 2 + 1;
-    real_split_kernel<<<(unsigned)((work + 255) / 256), 256, 0, s>>>((float2*)d_out, h, pl->n_user);
+    const int64_t h = pl->n, pairs = h / 2 + 1;
+    const int64_t threads = (pairs + SPLIT_K - 1) / SPLIT_K;
+    real_split_kernel<<<(unsigned)((threads + 255) / 256), 256, 0, s>>>((float2*)d_out, h, pl->n_user);
     CUDA_TRY(cudaGetLastError());
     if (ev) CUDA_TRY(cudaEventRecord(ev[pl->npass + 1], s));
   }

@@ -12,6 +12,9 @@ to the host), so parity never depends on two generators agreeing.
                                 frequencies + complex noise with VARIANCE 0.01
                                 per real component (std 0.1)
   C5  N = 2^32      complex128  re/im iid U(-1, 1), forward then inverse
+  R24, R27, R30     float32     the reference's own workload (bench.py:109-136):
+                                real input U[-0.5, 0.5), packed PERM output,
+                                N = 2^24, 2^27, 2^30
 """
 
 import math
@@ -24,6 +27,9 @@ CONFIGS = {
     "c3": dict(n=1 << 30, dtype="complex64", kind="normal", roundtrip=False),
     "c4": dict(n=3 << 28, dtype="complex128", kind="tones", roundtrip=False),
     "c5": dict(n=1 << 32, dtype="complex128", kind="uniform", roundtrip=True),
+    "r24": dict(n=1 << 24, dtype="float32", kind="uniform_half", roundtrip=False),
+    "r27": dict(n=1 << 27, dtype="float32", kind="uniform_half", roundtrip=False),
+    "r30": dict(n=1 << 30, dtype="float32", kind="uniform_half", roundtrip=False),
 }
 
 N_TONES = 16
@@ -46,8 +52,13 @@ def tone_frequencies(n: int, seed: int):
 
 
 def make_input(n: int, dtype: str, kind: str, seed: int, device="cuda"):
-    """Complex tensor of length n on `device` (torch)."""
+    """Complex (or, for dtype float32, real) tensor of length n on `device` (torch)."""
     import torch
+
+    if dtype == "float32":  # the reference's signal: U[-0.5, 0.5) float32 (bench.py:109-112)
+        g = torch.Generator(device=device)
+        g.manual_seed(seed)
+        return torch.rand(n, generator=g, device=device, dtype=torch.float32) - 0.5
 
     tdt = {"complex64": torch.complex64, "complex128": torch.complex128}[dtype]
     rdt = torch.float32 if dtype == "complex64" else torch.float64
