@@ -103,23 +103,31 @@ __device__ __forceinline__ int64_t t1_out(const Args& a, int j2, uint32_t k1) {
 
 // Position -> (sub-stage, group, task) of the claim order above (thread 0 only).
 __device__ __forceinline__ void decode(const Args& a, uint32_t pos, int& isB, int& g, int& task) {
-  const uint32_t L = a.lag, na = a.ntA, nb = a.ntB, per = na + nb, G = a.ngroups;
+  // Super-groups of W = a.wg adjacent column groups: the order is the
+  // group-level order of the super-groups with each block's tasks interleaved
+  // over its W groups, so W adjacent 128-byte segments of every row are read
+  // (and, in B, written) at about the same time -- DRAM page locality.
+  // lag counts super-groups; dependencies stay per group.
+  const uint32_t W = a.wg, L = a.lag, na = a.ntA * W, nb = a.ntB * W, per = na + nb, G = a.ngroups / W;
+  uint32_t sg, t;
   if (pos < L * na) {
     isB = 0;
-    g = (int)(pos / na);
-    task = (int)(pos % na);
+    sg = pos / na;
+    t = pos % na;
   } else if (pos < L * na + (G - L) * per) {
     const uint32_t q = pos - L * na;
     const uint32_t i = L + q / per, r = q % per;
     isB = r < nb;
-    g = (int)(isB ? i - L : i);
-    task = (int)(isB ? r : r - nb);
+    sg = isB ? i - L : i;
+    t = isB ? r : r - nb;
   } else {
     const uint32_t q = pos - L * na - (G - L) * per;
     isB = 1;
-    g = (int)(G - L + q / nb);
-    task = (int)(q % nb);
+    sg = G - L + q / nb;
+    t = q % nb;
   }
+  g = (int)(sg * W + t % W);
+  task = (int)(t / W);
 }
 
 // thread 0's synchronisation state
@@ -410,9 +418,11 @@ __global__ void __launch_bounds__(LT<R>::NT, MINB) lean_pass(const __grid_consta
         const uint64_t jg = (uint64_t)(a.j2off + j2);  // global column (sharded: rank offset)
         double2 w = wroot((int64_t)((jg * c) % (uint64_t)a.N), a.N);
         const double2 st = wroot((int64_t)((jg * (RA * QB)) % (uint64_t)a.N), a.N);
+        V* op = DST + (int64_t)j2 * a.R + c;
 #pragma unroll
         for (int kp = 0; kp < 16; ++kp) {
-          st_hint(DST + t1_out(a, j2, c + kp * (RA * QB)), cmul(v[P<16>(kp)], to_v(w, R())), pol);
+          V* dp = a.obl == 0 ? op + kp * (RA * QB) : DST + t1_out(a, j2, c + kp * (RA * QB));
+          st_hint(dp, cmul(v[P<16>(kp)], to_v(w, R())), pol);
           if (kp < 15) w = cmul(w, st);
         }
       } else {
@@ -655,12 +665,22 @@ __global__ void __launch_bounds__(pair::NT, 4) lean_pair(const __grid_constant__
         double2 w0 = wroot((int64_t)((jg * c) % N), a.N);
         const V wj = to_v(wroot((int64_t)(jg % N), a.N), 0.f);
         const double2 st = wroot((int64_t)((jg * (256 * QB)) % N), a.N);
+        if (a.obl == 0) {  // y[k1 + R j2]: one base pointer, immediate offsets
+          V* op = DST + (int64_t)j2 * a.R + c;
 #pragma unroll
-        for (int kp = 0; kp < 16; ++kp) {
-          const V w = to_v(w0, 0.f);
-          pair::st16(DST + t1_out(a, j2, c + kp * (256 * QB)), cmul(x[P<16>(kp)], w), cmul(y[P<16>(kp)], cmul(w, wj)),
-                     pol);
-          if (kp < 15) w0 = cmul(w0, st);
+          for (int kp = 0; kp < 16; ++kp) {
+            const V w = to_v(w0, 0.f);
+            pair::st16(op + kp * (256 * QB), cmul(x[P<16>(kp)], w), cmul(y[P<16>(kp)], cmul(w, wj)), pol);
+            if (kp < 15) w0 = cmul(w0, st);
+          }
+        } else {  // sharded NCCL path: blocked by destination rank
+#pragma unroll
+          for (int kp = 0; kp < 16; ++kp) {
+            const V w = to_v(w0, 0.f);
+            pair::st16(DST + t1_out(a, j2, c + kp * (256 * QB)), cmul(x[P<16>(kp)], w),
+                       cmul(y[P<16>(kp)], cmul(w, wj)), pol);
+            if (kp < 15) w0 = cmul(w0, st);
+          }
         }
       } else {
         const int kb = task * DB + dl;
@@ -798,18 +818,25 @@ static bool plan_pass(Pass& q, bool t1, int ra, int lb, int64_t cols, int64_t N,
   q.grid = occ * num_sms;
   // Claimed tasks in flight span about 3 grids: B(g) is issued `lag` groups
   // after A(g), and A(g) reuses the slot of group g - nslots.
-  const int64_t per = (int64_t)a.ntA + a.ntB;
+  // W adjacent groups interleaved (decode); lag in super-groups of W, slots in groups
+  int64_t W = 1;
+  if (const char* ev = getenv("EFFT_LEAN_W")) W = atoi(ev);
+  while (W > 1 && a.ngroups % W) W /= 2;
+  if (W < 1) W = 1;
+  a.wg = (int32_t)W;
+  const int64_t G = a.ngroups / W;
+  const int64_t per = ((int64_t)a.ntA + a.ntB) * W;
   const int64_t window = (4 * (int64_t)q.grid + per - 1) / per;
   int64_t lag = window + 1;
   if (const char* ev = getenv("EFFT_LEAN_LAG")) lag = atoi(ev);
-  int64_t slots = lag + (window + 1) / 2 + 2;
+  int64_t slots = lag + (window + 1) / 2 + 2;  // super-groups
   if (const char* ev = getenv("EFFT_LEAN_SLOTS")) slots = atoi(ev);
   if (lag < 1) lag = 1;
-  if (lag > a.ngroups) lag = a.ngroups;
+  if (lag > G) lag = G;
   if (slots < lag + 1) slots = lag + 1;
-  if (slots > a.ngroups) slots = a.ngroups;
+  if (slots > G) slots = G;
   a.lag = (int32_t)lag;
-  a.nslots = (int32_t)slots;
+  a.nslots = (int32_t)(slots * W);
   q.counter_ints = 2 + 2 * (int64_t)a.ngroups;
   return true;
 }

@@ -33,6 +33,7 @@ struct Args {
   int64_t slot_elems;  // F * R: one column group
   int64_t total;       // ngroups * (ntA + ntB) tasks
   int32_t ngroups, nslots, lag;
+  int32_t wg;          // adjacent column groups interleaved in the claim order (lag counts W-group blocks)
   int32_t ntA, ntB;    // tasks per group: A (RB, one per ja), B (RA * RB / 256)
   unsigned long long* ctr;
   int32_t* doneA;
