@@ -154,52 +154,74 @@ def _torch():
 
 
 class TransformHandle:
-    """Device buffers, pinned host views and the native plan for one TransformPlan."""
+    """Device buffers, pinned host views and the native plan for one TransformPlan.
+
+    Buffers are allocated on first use, each once for the handle's life: the
+    pinned host pair by ``data`` / ``result`` / ``run()``, the device pair by
+    ``run()`` / ``device_data`` / ``run_device()``.  A device-only user
+    (``execute_tensors`` on its own tensors) never pays for the mirrors -- at
+    C5 size each of the four arrays is 64 GiB."""
 
     def __init__(self, plan: TransformPlan):
         torch = _torch()
         self.plan = plan
         if not torch.cuda.is_available():
             raise RuntimeError("TransformHandle needs a CUDA device (there is no CPU fallback)")
-        dev = torch.device("cuda", plan.device)
+        self._dev = torch.device("cuda", plan.device)
         if plan.dtype == "float32":
             native_dtype = _native.EFFT_R32
-            tdt = torch.float32
+            self._tdt = torch.float32
         elif plan.dtype == "complex64":
-            native_dtype, tdt = _native.EFFT_C64, torch.complex64
+            native_dtype, self._tdt = _native.EFFT_C64, torch.complex64
         else:
-            native_dtype, tdt = _native.EFFT_C128, torch.complex128
+            native_dtype, self._tdt = _native.EFFT_C128, torch.complex128
         self._native = _native.NativePlan(plan.n, native_dtype, plan.direction, plan.device,
                                           _native.EFFT_FLAG_CHECK_FINITE)
+        self._dev_in = self._dev_out = None
+        self._data = self._result = None
+        self._closed = False
+
+    def _alloc(self, what):
+        torch = _torch()
         try:
-            self._dev_in = torch.zeros(plan.n, dtype=tdt, device=dev)
-            self._dev_out = torch.zeros(plan.n, dtype=tdt, device=dev)
-            self._host_in = torch.zeros(plan.n, dtype=tdt, pin_memory=True)
-            self._host_out = torch.zeros(plan.n, dtype=tdt, pin_memory=True)
-        except RuntimeError as exc:  # CUDA OOM
+            if what == "host" and self._host_in is None:
+                # contents before the first run are undefined in the reference (core.py:155);
+                # zero-filled here
+                self._host_in = torch.zeros(self.plan.n, dtype=self._tdt, pin_memory=True)
+                self._host_out = torch.zeros(self.plan.n, dtype=self._tdt, pin_memory=True)
+                self._data = self._host_in.numpy()
+                self._result = self._host_out.numpy().view()
+                self._result.setflags(write=False)
+            elif what == "device" and self._dev_in is None:
+                self._dev_in = torch.zeros(self.plan.n, dtype=self._tdt, device=self._dev)
+                self._dev_out = torch.zeros(self.plan.n, dtype=self._tdt, device=self._dev)
+        except RuntimeError as exc:  # CUDA OOM / pinning failure
             from .errors import AllocationFailure
 
-            self._native.close()
             raise AllocationFailure(str(exc)) from exc
-        self._data = self._host_in.numpy()
-        self._result = self._host_out.numpy().view()
-        self._result.setflags(write=False)
-        self._closed = False
 
     # -- reference surface -------------------------------------------------
     @property
     def data(self) -> np.ndarray:
         """Writable pinned host view of the input; preserved across transforms."""
+        if self._data is None:
+            self._check_open()
+            self._alloc("host")
         return self._data
 
     @property
     def result(self) -> np.ndarray:
         """Read-only pinned host view of the output of the last ``run()``."""
+        if self._result is None:
+            self._check_open()
+            self._alloc("host")
         return self._result
 
     def run(self) -> np.ndarray:
         """H2D copy of ``data``, the transform, D2H copy into ``result``."""
         self._check_open()
+        self._alloc("host")
+        self._alloc("device")
         torch = _torch()
         with torch.cuda.device(self.plan.device):
             stream = torch.cuda.current_stream()
@@ -235,16 +257,21 @@ class TransformHandle:
     @property
     def device_data(self):
         """Device input tensor (never written by a transform)."""
+        self._check_open()
+        self._alloc("device")
         return self._dev_in
 
     @property
     def device_result(self):
         """Device output tensor."""
+        self._check_open()
+        self._alloc("device")
         return self._dev_out
 
     def run_device(self, stream=None):
         """Enqueue the transform device_data -> device_result on `stream` (no copies, no sync)."""
         self._check_open()
+        self._alloc("device")
         torch = _torch()
         s = stream if stream is not None else torch.cuda.current_stream(self.plan.device)
         self._native.execute(self._dev_in.data_ptr(), self._dev_out.data_ptr(), s.cuda_stream)
@@ -256,7 +283,7 @@ class TransformHandle:
         torch = _torch()
         if src.numel() != self.plan.n or dst.numel() != self.plan.n:
             raise SizeMismatch(f"tensors must have {self.plan.n} elements")
-        if src.dtype != self._dev_in.dtype or dst.dtype != self._dev_in.dtype:
+        if src.dtype != self._tdt or dst.dtype != self._tdt:
             raise SizeMismatch("tensor dtype does not match the plan")
         if not (src.is_contiguous() and dst.is_contiguous()):
             raise SizeMismatch("tensors must be contiguous")
@@ -270,7 +297,8 @@ class TransformHandle:
         torch = _torch()
         if h_in.shape != (self.plan.n,) or h_out.shape != (self.plan.n,):
             raise SizeMismatch(f"host buffers must have length {self.plan.n}")
-        want = self._data.dtype
+        want = np.dtype({"float32": np.float32, "complex64": np.complex64, "complex128": np.complex128}[
+            self.plan.dtype])
         if h_in.dtype != want or h_out.dtype != want:
             raise SizeMismatch(f"host buffers must be {want} (the plan dtype)")
         if not (h_in.flags.c_contiguous and h_out.flags.c_contiguous):

@@ -45,6 +45,7 @@
 // relaxed loads, and ONE fence.acq_rel per tile, issued right after the tile
 // loads, releases the previous tile and completes those acquires.
 #include <algorithm>
+#include <type_traits>
 #include <cstdlib>
 
 #include "efft_kernels.cuh"
@@ -724,23 +725,27 @@ __global__ void __launch_bounds__(pair::NT, 4) lean_pair(const __grid_constant__
 // ---------------------------------------------------------------------------
 // host side
 // ---------------------------------------------------------------------------
+// 4 CTAs per SM for both types.  (The complex128 instantiations spill 8-12
+// bytes at this 128-register cap; measured at 3 CTAs per SM, ptxas spills
+// 44-76 bytes instead, so 4 stays.)
 template <typename R, int RA>
 static void* pick_ra(int rb, bool t1) {
+  constexpr int MB = 4;
   if constexpr (RA != 256) {  // the odd factor runs in the in-place pass only
     if (t1) return nullptr;
     switch (rb) {
-      case 32: return (void*)lean_pass<R, RA, 32, false, 4>;
-      case 64: return (void*)lean_pass<R, RA, 64, false, 4>;
-      case 128: return (void*)lean_pass<R, RA, 128, false, 4>;
-      case 256: return (void*)lean_pass<R, RA, 256, false, 4>;
+      case 32: return (void*)lean_pass<R, RA, 32, false, MB>;
+      case 64: return (void*)lean_pass<R, RA, 64, false, MB>;
+      case 128: return (void*)lean_pass<R, RA, 128, false, MB>;
+      case 256: return (void*)lean_pass<R, RA, 256, false, MB>;
       default: return nullptr;
     }
   } else {
     switch (rb) {
-      case 32: return t1 ? (void*)lean_pass<R, RA, 32, true, 4> : (void*)lean_pass<R, RA, 32, false, 4>;
-      case 64: return t1 ? (void*)lean_pass<R, RA, 64, true, 4> : (void*)lean_pass<R, RA, 64, false, 4>;
-      case 128: return t1 ? (void*)lean_pass<R, RA, 128, true, 4> : (void*)lean_pass<R, RA, 128, false, 4>;
-      case 256: return t1 ? (void*)lean_pass<R, RA, 256, true, 4> : (void*)lean_pass<R, RA, 256, false, 4>;
+      case 32: return t1 ? (void*)lean_pass<R, RA, 32, true, MB> : (void*)lean_pass<R, RA, 32, false, MB>;
+      case 64: return t1 ? (void*)lean_pass<R, RA, 64, true, MB> : (void*)lean_pass<R, RA, 64, false, MB>;
+      case 128: return t1 ? (void*)lean_pass<R, RA, 128, true, MB> : (void*)lean_pass<R, RA, 128, false, MB>;
+      case 256: return t1 ? (void*)lean_pass<R, RA, 256, true, MB> : (void*)lean_pass<R, RA, 256, false, MB>;
       default: return nullptr;
     }
   }
