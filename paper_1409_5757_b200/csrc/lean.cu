@@ -722,6 +722,285 @@ __global__ void __launch_bounds__(pair::NT, 4) lean_pair(const __grid_constant__
 #undef STG
 }
 
+// Wide complex64 tile kernel: F = 32 columns per group, so every HBM access
+// is a 256-byte segment (tools/skel_bench.cu: a strided read + strided write
+// pass reaches 5.9 TB/s with 256-byte segments vs 4.4 TB/s with 128-byte
+// ones).  64 KB tiles, 256 threads, 32 points per thread (two adjacent
+// columns, 16-byte lanes), one 64 KB shared-memory exchange per sub-stage,
+// two CTAs per SM; scheduling as lean_pair (Sched).
+//   A tile:  thread (column pair cp < 16, s < 16), rows jb = s + 16 t
+//   T0 B:    ring [kb][ja][32 lanes], tile = DB kb x RB ja x 32 columns
+//   T1 B:    ring [j2l][ja][ks][kt], tile = 2 ks x 16 kt x RB ja x DB columns,
+//            task = (ks pair ksp, column block jblk): 32 consecutive k1 per column
+namespace wide {
+constexpr int NT = 256;
+constexpr int KP = 33, SP = 16 * KP + 1;  // float2 pitches of the transposing A exchange [s][kt][j2]
+constexpr int XB1 = 16 * SP;              // 8464 float2
+constexpr int SMEM_T1 = XB1 * 8 + 512 * 8;
+constexpr int SMEM_T0 = 8192 * 8 + 512 * 8;
+}  // namespace wide
+
+template <int RB, bool T1>
+__device__ __forceinline__ int wide_b_line(int task, int dl, int p, int q, int ksl) {
+  constexpr int QB = RB / 16, DB = 16 / QB;
+  const int ja = p + 16 * q;
+  if constexpr (T1)  // ring [j2l][ja][ks][kt]; task = (ksp = task & 7, jblk = task >> 3)
+    return ((((task >> 3) * DB + dl) * RB + ja) * 16 + 2 * (task & 7) + ksl) * 16;
+  else  // ring [kb][ja][32 lanes]
+    return ((task * DB + dl) * RB + ja) * 32;
+}
+
+template <int RB, bool T1>
+__global__ void __launch_bounds__(wide::NT, 2) lean_wide(const __grid_constant__ Args a) {
+  using V = float2;
+  constexpr int QB = RB / 16, DB = 16 / QB;
+  extern __shared__ __align__(128) unsigned char smraw[];
+  V* xb = reinterpret_cast<V*>(smraw);
+  float4* xq = reinterpret_cast<float4*>(smraw);
+  V* w256 = xb + (T1 ? wide::XB1 : 8192);
+  V* wlo = w256 + 256;
+  __shared__ SchedShared shs;
+  const int tid = threadIdx.x;
+#define SRC reinterpret_cast<const V*>(a.src)
+#define DST reinterpret_cast<V*>(a.dst)
+#define STG reinterpret_cast<V*>(a.stg)
+  for (int i = tid; i < 256; i += wide::NT) {
+    w256[i] = to_v(wroot(i, 256), 0.f);
+    wlo[i] = to_v(wroot(i, a.R), 0.f);
+  }
+  Sched sc{&shs};
+  sc.init(a);
+  bool nf = false;
+  int isB, g, task;
+  while (sc.next(a, isB, g, task)) {
+    V* sp = STG + (int64_t)(g % a.nslots) * a.slot_elems;
+    V x[16], y[16];  // columns 2cp (x) and 2cp + 1 (y)
+    // thread roles
+    //   A: T0 cp = tid & 15, s = tid >> 4;  T1 (bank-conflict-free STS.64 halves):
+    //      cp = (tid & 7) + 8 ((tid >> 5) & 1), s = 4 (tid >> 6) + ((tid >> 3) & 3)
+    //   B: T0 cp = tid & 15, p = tid >> 4;  T1 cp = tid & 7 (kt pair), ksl = (tid >> 3) & 1, p = tid >> 4
+    int cp, r, ksl = 0;
+    if (!isB) {
+      if constexpr (T1) {
+        cp = (tid & 7) + 8 * ((tid >> 5) & 1);
+        r = 4 * (tid >> 6) + ((tid >> 3) & 3);
+      } else {
+        cp = tid & 15;
+        r = tid >> 4;
+      }
+    } else {
+      if constexpr (T1) {
+        cp = tid & 7;
+        ksl = (tid >> 3) & 1;
+      } else {
+        cp = tid & 15;
+      }
+      r = tid >> 4;
+    }
+    if (isB) {
+#pragma unroll
+      for (int dl = 0; dl < DB; ++dl)
+#pragma unroll
+        for (int q = 0; q < QB; ++q) {
+          const float4 t = pair::ld16_l2(sp + wide_b_line<RB, T1>(task, dl, r, q, ksl) + 2 * cp);
+          x[dl * QB + q] = make_float2(t.x, t.y);
+          y[dl * QB + q] = make_float2(t.z, t.w);
+        }
+    } else {  // A: jb = s + 16 t with s = r
+      const uint64_t pol = policy_evict_first();
+      const V* p0 = SRC + (int64_t)g * 32 + 2 * cp + a.LS * (int64_t)(task + RB * r);
+      const int64_t step = a.LS * (int64_t)(RB * 16);
+#pragma unroll
+      for (int t = 0; t < 16; ++t) {
+        const float4 u = pair::ld16_hbm(p0 + t * step, pol);
+        x[t] = make_float2(u.x, u.y);
+        y[t] = make_float2(u.z, u.w);
+      }
+    }
+    sc.after_loads(a, isB, g);
+    if (isB) {
+      // ---- B stage 0: W_R^(ja kb), QB-point DFTs over q
+#pragma unroll
+      for (int dl = 0; dl < DB; ++dl) {
+        const int kb = T1 ? 2 * cp + 16 * (2 * (task & 7) + ksl) : task * DB + dl;
+        const int e0 = r * kb, es = 16 * kb;  // < R
+        V w = cmul(w256[(e0 >> 8) * (256 / RB)], wlo[e0 & 255]);
+        const V st = cmul(w256[(es >> 8) * (256 / RB)], wlo[es & 255]);
+        if constexpr (T1) {
+          const int e1 = e0 + r, es1 = es + 16;  // kb + 1
+          V w1 = cmul(w256[(e1 >> 8) * (256 / RB)], wlo[e1 & 255]);
+          const V st1 = cmul(w256[(es1 >> 8) * (256 / RB)], wlo[es1 & 255]);
+#pragma unroll
+          for (int q = 0; q < QB; ++q) {
+            x[dl * QB + q] = cmul(x[dl * QB + q], w);
+            y[dl * QB + q] = cmul(y[dl * QB + q], w1);
+            if (q + 1 < QB) {
+              w = cmul(w, st);
+              w1 = cmul(w1, st1);
+            }
+          }
+        } else {
+#pragma unroll
+          for (int q = 0; q < QB; ++q) {
+            x[dl * QB + q] = cmul(x[dl * QB + q], w);
+            y[dl * QB + q] = cmul(y[dl * QB + q], w);
+            if (q + 1 < QB) w = cmul(w, st);
+          }
+        }
+      }
+#pragma unroll
+      for (int dl = 0; dl < DB; ++dl) {
+        reg_dft<float, QB>(x + dl * QB);
+        reg_dft<float, QB>(y + dl * QB);
+      }
+      {  // W_RB^(p kq)
+        const V* wp = w256;
+#pragma unroll
+        for (int k = 1; k < QB; ++k) {
+          wp += r * (256 / RB);
+          const V w = *wp;
+#pragma unroll
+          for (int dl = 0; dl < DB; ++dl) {
+            x[dl * QB + P<QB>(k)] = cmul(x[dl * QB + P<QB>(k)], w);
+            y[dl * QB + P<QB>(k)] = cmul(y[dl * QB + P<QB>(k)], w);
+          }
+        }
+      }
+      // consumed staging lines leave L2 without write-back: a 128-byte line is
+      // read by the 8 lanes of one warp; each of them drops two
+      {
+        const int own = cp & 7, half = T1 ? 0 : (cp >> 3);
+#pragma unroll
+        for (int i = own; i < 16; i += 8) l2_discard(sp + wide_b_line<RB, T1>(task, i / QB, r, i % QB, ksl) + 16 * half);
+      }
+#pragma unroll
+      for (int dl = 0; dl < DB; ++dl)
+#pragma unroll
+        for (int k = 0; k < QB; ++k) {
+          const V u = x[dl * QB + P<QB>(k)], w = y[dl * QB + P<QB>(k)];
+          if constexpr (T1)  // [ksl][dl][kq][p][8 kt pairs]
+            xq[(((ksl * DB + dl) * QB + k) * 16 + r) * 8 + cp] = make_float4(u.x, u.y, w.x, w.y);
+          else  // [dl][kq][p][16 pairs]
+            xq[((dl * QB + k) * 16 + r) * 16 + cp] = make_float4(u.x, u.y, w.x, w.y);
+        }
+    } else {
+      // ---- A stage 0: 16-point DFTs over t, W_256^(s kt) shared by the pair
+      if (a.check_finite) {
+#pragma unroll
+        for (int t = 0; t < 16; ++t)
+          nf |= !(isfinite(x[t].x) && isfinite(x[t].y) && isfinite(y[t].x) && isfinite(y[t].y));
+      }
+      if constexpr (T1) {
+        const V ci = cvt(a.cin, 0.f);
+#pragma unroll
+        for (int t = 0; t < 16; ++t) {
+          x[t] = mul2(x[t], ci);
+          y[t] = mul2(y[t], ci);
+        }
+      }
+      reg_dft<float, 16>(x);
+      reg_dft<float, 16>(y);
+      {
+        const V* wp = w256;
+#pragma unroll
+        for (int k = 1; k < 16; ++k) {
+          wp += r;
+          const V w = *wp;
+          x[P<16>(k)] = cmul(x[P<16>(k)], w);
+          y[P<16>(k)] = cmul(y[P<16>(k)], w);
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < 16; ++k) {
+        if constexpr (T1) {  // [s][kt][j2]: s pitch SP, kt pitch KP (odd: two STS.64)
+          xb[r * wide::SP + k * wide::KP + 2 * cp] = x[P<16>(k)];
+          xb[r * wide::SP + k * wide::KP + 2 * cp + 1] = y[P<16>(k)];
+        } else {  // [kt][s][16 pairs]
+          const V u = x[P<16>(k)], w = y[P<16>(k)];
+          xq[(k * 16 + r) * 16 + cp] = make_float4(u.x, u.y, w.x, w.y);
+        }
+      }
+    }
+    sc.before_exchange(a, g);
+    __syncthreads();
+    if (isB) {
+      // ---- B stage 1: 16-point DFTs over p; thread (cp, [ksl], dl, kq), r = tid >> 4
+      const int kq = r % QB, dl = r / QB;
+#pragma unroll
+      for (int u = 0; u < 16; ++u) {
+        const float4 t = T1 ? xq[(((ksl * DB + dl) * QB + kq) * 16 + u) * 8 + cp] : xq[((dl * QB + kq) * 16 + u) * 16 + cp];
+        x[u] = make_float2(t.x, t.y);
+        y[u] = make_float2(t.z, t.w);
+      }
+      reg_dft<float, 16>(x);
+      reg_dft<float, 16>(y);
+      const uint64_t pol = policy_evict_first();
+      if constexpr (T1) {
+        // y[k1 + R1 j2] = Y W_N^(j2 k1), k1 = kt + 16 ks + 256 kq + 256 QB kp, kt = 2cp (+1), ks = 2 ksp + ksl
+        const int j2 = g * 32 + (task >> 3) * DB + dl;
+        const uint32_t c = (uint32_t)(2 * cp + 16 * (2 * (task & 7) + ksl) + 256 * kq);
+        // W_N^(j2 k1): fp64 base and step from exact exponents, fp64 recurrence, one rounding per use
+        const uint64_t N = (uint64_t)a.N, jg = (uint64_t)(a.j2off + j2);
+        double2 w0 = wroot((int64_t)((jg * c) % N), a.N);
+        const V wj = to_v(wroot((int64_t)(jg % N), a.N), 0.f);
+        const double2 st = wroot((int64_t)((jg * (256 * QB)) % N), a.N);
+        if (a.obl == 0) {
+          V* op = DST + (int64_t)j2 * a.R + c;
+#pragma unroll
+          for (int kp = 0; kp < 16; ++kp) {
+            const V w = to_v(w0, 0.f);
+            pair::st16(op + kp * (256 * QB), cmul(x[P<16>(kp)], w), cmul(y[P<16>(kp)], cmul(w, wj)), pol);
+            if (kp < 15) w0 = cmul(w0, st);
+          }
+        } else {
+#pragma unroll
+          for (int kp = 0; kp < 16; ++kp) {
+            const V w = to_v(w0, 0.f);
+            pair::st16(DST + t1_out(a, j2, c + kp * (256 * QB)), cmul(x[P<16>(kp)], w),
+                       cmul(y[P<16>(kp)], cmul(w, wj)), pol);
+            if (kp < 15) w0 = cmul(w0, st);
+          }
+        }
+      } else {
+        const int kb = task * DB + dl;
+        const V co = cvt(a.cout, 0.f);
+        V* op = DST + (int64_t)g * 32 + 2 * cp + a.LS * (int64_t)(kb + 256 * kq);
+        const int64_t step = a.LS * (int64_t)(256 * QB);
+#pragma unroll
+        for (int kp = 0; kp < 16; ++kp) pair::st16(op + kp * step, mul2(x[P<16>(kp)], co), mul2(y[P<16>(kp)], co), pol);
+      }
+    } else {
+      // ---- A stage 1: 16-point DFTs over s -> ks, store to the ring
+      //   T0 thread (pair cp = tid & 15, kt = tid >> 4): ring [kb][ja][32 lanes], kb = kt + 16 ks
+      //   T1 thread (kt pair ktp = tid & 7, j2l = tid >> 3): ring [j2l][ja][ks][kt]
+      const int c0 = T1 ? (tid & 7) : (tid & 15), r1 = T1 ? (tid >> 3) : (tid >> 4);
+#pragma unroll
+      for (int u = 0; u < 16; ++u) {
+        if constexpr (T1) {
+          x[u] = xb[u * wide::SP + (2 * c0) * wide::KP + r1];
+          y[u] = xb[u * wide::SP + (2 * c0 + 1) * wide::KP + r1];
+        } else {
+          const float4 t = xq[(r1 * 16 + u) * 16 + c0];
+          x[u] = make_float2(t.x, t.y);
+          y[u] = make_float2(t.z, t.w);
+        }
+      }
+      reg_dft<float, 16>(x);
+      reg_dft<float, 16>(y);
+      const int base = T1 ? (r1 * RB + task) * 256 + 2 * c0 : (r1 * RB + task) * 32 + 2 * c0;
+      const int step = T1 ? 16 : 16 * RB * 32;
+      const uint64_t keep = policy_evict_last();
+#pragma unroll
+      for (int ks = 0; ks < 16; ++ks) pair::st16(sp + base + ks * step, x[P<16>(ks)], y[P<16>(ks)], keep);
+    }
+    sc.end(a, isB, g);
+  }
+  sc.finish(a, nf);
+#undef SRC
+#undef DST
+#undef STG
+}
+
 // ---------------------------------------------------------------------------
 // host side
 // ---------------------------------------------------------------------------
@@ -771,6 +1050,23 @@ static void* pick_pair(int rb, bool t1) {
     default: return nullptr;
   }
 }
+static void* pick_wide(int rb, bool t1) {
+  switch (rb) {
+    case 32: return t1 ? (void*)lean_wide<32, true> : (void*)lean_wide<32, false>;
+    case 64: return t1 ? (void*)lean_wide<64, true> : (void*)lean_wide<64, false>;
+    case 128: return t1 ? (void*)lean_wide<128, true> : (void*)lean_wide<128, false>;
+    case 256: return t1 ? (void*)lean_wide<256, true> : (void*)lean_wide<256, false>;
+    default: return nullptr;
+  }
+}
+// EFFT_LEAN_WIDE: bit 0 = the transposing pass, bit 1 = the in-place pass.
+// Default 2 (measured at 2^30: in-place pass 4.93-4.94 vs 5.02-5.03 ms with the
+// paired kernel; the transposing pass is 5.74 vs 5.39 ms wide, so it stays paired)
+static bool use_wide(bool t1) {
+  const char* e = getenv("EFFT_LEAN_WIDE");
+  const int v = e ? atoi(e) : 2;
+  return (v >> (t1 ? 0 : 1)) & 1;
+}
 static bool use_pair() {
   static const int v = getenv("EFFT_LEAN_PAIR") ? atoi(getenv("EFFT_LEAN_PAIR")) : 1;
   return v != 0;
@@ -781,20 +1077,26 @@ static bool use_pair() {
 // W_N^((j2off + j2) k1).  Returns false when no kernel covers it.
 static bool plan_pass(Pass& q, bool t1, int ra, int lb, int64_t cols, int64_t N, int64_t j2off, int c128,
                       int inverse, bool scale_inverse, bool check_finite, int num_sms, int* err_cuda) {
-  const int F = c128 ? 8 : 16, NT = 16 * F;
+  // complex64, RA = 256: the wide kernel (32-column groups, 256-byte segments)
+  // when enabled and the columns divide, else the paired one (16 columns)
+  const bool wide = !c128 && ra == 256 && lb >= 5 && use_wide(t1) && cols % 32 == 0;
+  const int F = wide ? 32 : c128 ? 8 : 16, NT = 16 * F;
   const size_t elem = c128 ? 16 : 8;
   if (cols < F || cols % F) return false;
   q.ra = ra;
   q.rb = 1 << lb;
   const int64_t R = (int64_t)ra << lb;
-  const bool paired = !c128 && q.ra == 256 && use_pair();
-  q.fn = reinterpret_cast<void (*)(Args)>(paired ? pick_pair(q.rb, t1)
+  const bool paired = !wide && !c128 && q.ra == 256 && use_pair();
+  q.fn = reinterpret_cast<void (*)(Args)>(wide ? pick_wide(q.rb, t1)
+                                          : paired ? pick_pair(q.rb, t1)
                                           : c128 ? pick<double>(q.ra, q.rb, t1) : pick<float>(q.ra, q.rb, t1));
   if (!q.fn) return false;
-  q.nt = paired ? pair::NT : NT;
+  q.nt = wide ? wide::NT : paired ? pair::NT : NT;
+  q.wide = wide;
   // exchange (padded only in the transposing pass) + W_256 + W_R^(i<256) (+ two 192-entry tables)
-  q.smem = paired ? (int)(((t1 ? pair::XB2 : 4096) + 512) * elem)
-                  : (int)(((t1 ? 256 * (F + 1) : 256 * F) + 512 + (q.ra == 256 ? 0 : 2 * q.ra)) * elem);
+  q.smem = wide ? (t1 ? wide::SMEM_T1 : wide::SMEM_T0)
+                : paired ? (int)(((t1 ? pair::XB2 : 4096) + 512) * elem)
+                         : (int)(((t1 ? 256 * (F + 1) : 256 * F) + 512 + (q.ra == 256 ? 0 : 2 * q.ra)) * elem);
   Args& a = q.a;
   a = Args{};
   a.R = R;
@@ -803,7 +1105,7 @@ static bool plan_pass(Pass& q, bool t1, int ra, int lb, int64_t cols, int64_t N,
   a.LS = cols;
   a.ngroups = (int32_t)(cols / F);
   a.ntA = q.rb;
-  a.ntB = q.ra * q.rb / 256;
+  a.ntB = wide ? q.rb : q.ra * q.rb / 256;  // wide B tiles: 64 KB as well
   a.slot_elems = (int64_t)F * R;
   a.total = (int64_t)a.ngroups * (a.ntA + a.ntB);
   a.cin = make_double2(1.0, t1 && inverse ? -1.0 : 1.0);
@@ -834,7 +1136,7 @@ static bool plan_pass(Pass& q, bool t1, int ra, int lb, int64_t cols, int64_t N,
   const int64_t window = (4 * (int64_t)q.grid + per - 1) / per;
   int64_t lag = window + 1;
   if (const char* ev = getenv("EFFT_LEAN_LAG")) lag = atoi(ev);
-  int64_t slots = lag + (window + 1) / 2 + 2;  // super-groups
+  int64_t slots = wide ? lag + 3 : lag + (window + 1) / 2 + 2;  // super-groups (wide: 8 MB slots, keep <= ~80 MB)
   if (const char* ev = getenv("EFFT_LEAN_SLOTS")) slots = atoi(ev);
   if (lag < 1) lag = 1;
   if (lag > G) lag = G;

@@ -49,6 +49,7 @@ struct Pass {
   void (*fn)(Args);
   int grid, nt, smem;
   int ra, rb;
+  bool wide = false;  // 32-column groups (lean_wide)
   int64_t counter_ints;  // 2 (task counter) + 2 * ngroups
 };
 
