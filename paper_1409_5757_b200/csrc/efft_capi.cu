@@ -608,13 +608,18 @@ int finish_plan(efft_plan_s* pl) {
   }
   if (pl->lean) {
     int64_t off = 0;
-    for (auto& q : pl->lp) {
+    for (int i = 0; i < 2; ++i) {
+      auto& q = pl->lp[i];
       q.a.stg = pl->staging;
       q.a.ctr = reinterpret_cast<unsigned long long*>(pl->counters + off);
       q.a.doneA = pl->counters + off + 2;
       q.a.doneB = q.a.doneA + q.a.ngroups;
       q.a.flag = pl->flag;
       off += q.counter_ints;
+      if (q.pf && i == 0 && efft::lean::encode_ring(q, pl->staging) != 0) {
+        efft_plan_destroy(pl);
+        return fail(EFFT_ERR_CUDA, "tensor map (lean prefetch ring) encode failed");
+      }
     }
     return EFFT_OK;
   }
@@ -868,8 +873,11 @@ int efft_execute(efft_plan_t pl, const void* d_in, void* d_out, void* stream) {
   for (int p = 0; pl->lean && p < 2; ++p) {
     if (ev) CUDA_TRY(cudaEventRecord(ev[p], s));
     efft::lean::Pass& q = pl->lp[p];
+    const void* src = p == 0 ? d_in : d_out;
+    if (q.pf && q.mapA_ptr != src && efft::lean::encode_input(q, src) != 0)
+      return fail(EFFT_ERR_CUDA, "tensor map (lean prefetch input) encode failed");
     efft::lean::Args a = q.a;
-    a.src = p == 0 ? d_in : d_out;
+    a.src = src;
     a.dst = d_out;
     q.fn<<<q.grid, q.nt, q.smem, s>>>(a);
     CUDA_TRY(cudaGetLastError());

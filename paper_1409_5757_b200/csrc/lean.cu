@@ -496,16 +496,23 @@ __device__ __forceinline__ int pair_b_line(int task, int dl, int p, int q) {
     return ((task * DB + dl) * RB + ja) * 16;
 }
 
-template <int RB, bool T1>
-__global__ void __launch_bounds__(pair::NT, 4) lean_pair(const __grid_constant__ Args a) {
+// PF: the next tile is prefetched by TMA into a 32 KB landing buffer while
+// this one is computed (3 CTAs per SM); otherwise tiles are loaded straight
+// into registers (4 CTAs per SM).
+template <int RB, bool T1, bool PF>
+__global__ void __launch_bounds__(pair::NT, PF ? 3 : 4) lean_pair(const __grid_constant__ Args a) {
   using V = float2;
   constexpr int QB = RB / 16, DB = 16 / QB;
-  extern __shared__ __align__(128) unsigned char smraw[];
-  V* xb = reinterpret_cast<V*>(smraw);
-  float4* xq = reinterpret_cast<float4*>(smraw);
+  extern __shared__ __align__(1024) unsigned char smraw[];
+  unsigned char* const land = smraw;  // PF: 32 KB, 1024-aligned (128B-swizzled A boxes)
+  unsigned char* const xbase = smraw + (PF ? 32768 : 0);
+  V* xb = reinterpret_cast<V*>(xbase);
+  float4* xq = reinterpret_cast<float4*>(xbase);
   V* w256 = xb + (T1 ? pair::XB2 : 4096);  // the plain exchange needs no padding
   V* wlo = w256 + 256;
   __shared__ SchedShared shs;
+  __shared__ __align__(8) uint64_t lbar;
+  __shared__ int pf_sh[2];
   const int tid = threadIdx.x, cp = tid % 8, r = tid / 8;
 #define SRC reinterpret_cast<const V*>(a.src)
 #define DST reinterpret_cast<V*>(a.dst)
@@ -514,14 +521,61 @@ __global__ void __launch_bounds__(pair::NT, 4) lean_pair(const __grid_constant__
     w256[i] = to_v(wroot(i, 256), 0.f);
     wlo[i] = to_v(wroot(i, a.R), 0.f);
   }
+  if (PF && tid == 0) {
+    mbar_init(&lbar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    pf_sh[0] = pf_sh[1] = 0;
+  }
   Sched sc{&shs};
   sc.init(a);
   bool nf = false;
+  uint32_t lphase = 0;
   int isB, g, task;
+  // PF: one TMA for a whole tile (thread 0).  A: box {16 columns, 1, 256 rows}
+  // of the pass input, 128-byte swizzled; B: the tile's lines of the ring
+  // (T0: one contiguous 32 KB block; T1: box {16 kt, 1 ks, RB ja, DB columns}).
+  auto issue = [&](int tb, int tg, int tt) {
+    asm volatile("fence.proxy.async.global;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    mbar_arrive_tx(&lbar, 32768);
+    const uint64_t pol = policy_evict_first();
+    if (!tb) {
+      tma_load_3d(land, &a.mapA, tg * 16, tt, 0, &lbar, pol);
+    } else if constexpr (T1) {
+      tma_load_5d(land, &a.mapB, 0, tt & 15, 0, (tt >> 4) * DB, tg % a.nslots, &lbar, pol);
+    } else {
+      const V* src = STG + (int64_t)(tg % a.nslots) * a.slot_elems + (int64_t)(tt * DB) * RB * 16;
+      bulk_g2s(land, src, 32768, &lbar, pol);
+    }
+  };
   while (sc.next(a, isB, g, task)) {
     V* sp = STG + (int64_t)(g % a.nslots) * a.slot_elems;
     V x[16], y[16];  // columns 2cp (x) and 2cp + 1 (y)
-    if (isB) {
+    if constexpr (PF) {
+      if (tid == 0 && !pf_sh[sc.cb]) issue(isB, g, task);  // not prefetched (first tile, or late producers)
+      mbar_wait(&lbar, lphase);
+      lphase ^= 1;
+      const float4* L = reinterpret_cast<const float4*>(land);
+      if (isB) {  // [dl][ja][16 lanes] rows of 128 bytes
+#pragma unroll
+        for (int dl = 0; dl < DB; ++dl)
+#pragma unroll
+          for (int q = 0; q < QB; ++q) {
+            const float4 t = L[(dl * RB + r + 16 * q) * 8 + cp];
+            x[dl * QB + q] = make_float2(t.x, t.y);
+            y[dl * QB + q] = make_float2(t.z, t.w);
+          }
+      } else {  // [jb][16 columns], 16-byte chunk c of row jb at c ^ (jb & 7)
+#pragma unroll
+        for (int t = 0; t < 16; ++t) {
+          const int jb = r + 16 * t;
+          const float4 u = L[jb * 8 + (cp ^ (jb & 7))];
+          x[t] = make_float2(u.x, u.y);
+          y[t] = make_float2(u.z, u.w);
+        }
+      }
+      __syncthreads();  // the landing buffer is free
+    } else if (isB) {
 #pragma unroll
       for (int dl = 0; dl < DB; ++dl)
 #pragma unroll
@@ -542,6 +596,17 @@ __global__ void __launch_bounds__(pair::NT, 4) lean_pair(const __grid_constant__
       }
     }
     sc.after_loads(a, isB, g);
+    if constexpr (PF) {
+      // thread 0, after the fence that acquired the probe of the next task's
+      // producers: prefetch it when they are done (always for A tiles)
+      if (tid == 0) {
+        const int nb = sc.cb ^ 1;
+        const bool ok = shs.pos[nb] < a.total && (!shs.isB[nb] || sc.nxt_val >= a.ntA);
+        pf_sh[nb] = ok;
+        if (ok) issue(shs.isB[nb], shs.g[nb], shs.task[nb]);
+        pf_sh[sc.cb] = 0;  // this slot is re-published with the task after next
+      }
+    }
     if (isB) {
       // ---- B stage 0: W_R^(ja kb) (T0: one kb per dl, shared by the pair;
       // T1: kb = kt + 16 ks differs between the columns), QB-point DFTs
@@ -1040,15 +1105,23 @@ static void* pick(int ra, int rb, bool t1) {
     default: return pick_ra<R, 256>(rb, t1);
   }
 }
-static void* pick_pair(int rb, bool t1) {
+template <bool PF>
+static void* pick_pair_(int rb, bool t1) {
   switch (rb) {
-    case 16: return t1 ? (void*)lean_pair<16, true> : (void*)lean_pair<16, false>;
-    case 32: return t1 ? (void*)lean_pair<32, true> : (void*)lean_pair<32, false>;
-    case 64: return t1 ? (void*)lean_pair<64, true> : (void*)lean_pair<64, false>;
-    case 128: return t1 ? (void*)lean_pair<128, true> : (void*)lean_pair<128, false>;
-    case 256: return t1 ? (void*)lean_pair<256, true> : (void*)lean_pair<256, false>;
+    case 16: return t1 ? (void*)lean_pair<16, true, PF> : (void*)lean_pair<16, false, PF>;
+    case 32: return t1 ? (void*)lean_pair<32, true, PF> : (void*)lean_pair<32, false, PF>;
+    case 64: return t1 ? (void*)lean_pair<64, true, PF> : (void*)lean_pair<64, false, PF>;
+    case 128: return t1 ? (void*)lean_pair<128, true, PF> : (void*)lean_pair<128, false, PF>;
+    case 256: return t1 ? (void*)lean_pair<256, true, PF> : (void*)lean_pair<256, false, PF>;
     default: return nullptr;
   }
+}
+static void* pick_pair(int rb, bool t1, bool pf) { return pf ? pick_pair_<true>(rb, t1) : pick_pair_<false>(rb, t1); }
+// EFFT_LEAN_PF: bit 0 = prefetching pair kernel in the transposing pass, bit 1 = in the in-place pass
+static bool use_pf(bool t1) {
+  const char* e = getenv("EFFT_LEAN_PF");
+  const int v = e ? atoi(e) : 0;
+  return (v >> (t1 ? 0 : 1)) & 1;
 }
 static void* pick_wide(int rb, bool t1) {
   switch (rb) {
@@ -1076,7 +1149,8 @@ static bool use_pair() {
 // stride cols), t1 = the transposing pass with the four-step twiddle
 // W_N^((j2off + j2) k1).  Returns false when no kernel covers it.
 static bool plan_pass(Pass& q, bool t1, int ra, int lb, int64_t cols, int64_t N, int64_t j2off, int c128,
-                      int inverse, bool scale_inverse, bool check_finite, int num_sms, int* err_cuda) {
+                      int inverse, bool scale_inverse, bool check_finite, int num_sms, int* err_cuda,
+                      bool allow_pf = true) {
   // complex64, RA = 256: the wide kernel (32-column groups, 256-byte segments)
   // when enabled and the columns divide, else the paired one (16 columns)
   const bool wide = !c128 && ra == 256 && lb >= 5 && use_wide(t1) && cols % 32 == 0;
@@ -1087,15 +1161,16 @@ static bool plan_pass(Pass& q, bool t1, int ra, int lb, int64_t cols, int64_t N,
   q.rb = 1 << lb;
   const int64_t R = (int64_t)ra << lb;
   const bool paired = !wide && !c128 && q.ra == 256 && use_pair();
+  q.pf = paired && use_pf(t1) && allow_pf;  // (the sharded entries launch without tensor maps)
   q.fn = reinterpret_cast<void (*)(Args)>(wide ? pick_wide(q.rb, t1)
-                                          : paired ? pick_pair(q.rb, t1)
+                                          : paired ? pick_pair(q.rb, t1, q.pf)
                                           : c128 ? pick<double>(q.ra, q.rb, t1) : pick<float>(q.ra, q.rb, t1));
   if (!q.fn) return false;
   q.nt = wide ? wide::NT : paired ? pair::NT : NT;
   q.wide = wide;
   // exchange (padded only in the transposing pass) + W_256 + W_R^(i<256) (+ two 192-entry tables)
   q.smem = wide ? (t1 ? wide::SMEM_T1 : wide::SMEM_T0)
-                : paired ? (int)(((t1 ? pair::XB2 : 4096) + 512) * elem)
+                : paired ? (int)(((t1 ? pair::XB2 : 4096) + 512) * elem) + (q.pf ? 32768 : 0)
                          : (int)(((t1 ? 256 * (F + 1) : 256 * F) + 512 + (q.ra == 256 ? 0 : 2 * q.ra)) * elem);
   Args& a = q.a;
   a = Args{};
@@ -1211,8 +1286,8 @@ bool plan_sharded(int64_t n, int G, int rank, int c128, int inverse, bool check_
   const int64_t L1 = N1 / G, L2 = N2 / G;
   // pass 1 over this rank's L2 columns (global columns rank * L2 + c), pass 2 over its L1 columns
   if (!plan_pass(p[0], true, 256, lb1, L2, n, (int64_t)rank * L2, c128, inverse, true, check_finite, num_sms,
-                 err_cuda) ||
-      !plan_pass(p[1], false, ra2, lb2, L1, n, 0, c128, inverse, true, check_finite, num_sms, err_cuda))
+                 err_cuda, false) ||
+      !plan_pass(p[1], false, ra2, lb2, L1, n, 0, c128, inverse, true, check_finite, num_sms, err_cuda, false))
     return false;
   if (blocked) {
     int lg = 0;
@@ -1222,6 +1297,54 @@ bool plan_sharded(int64_t n, int G, int rank, int c128, int inverse, bool check_
   }
   *staging_elems = std::max(p[0].a.nslots * p[0].a.slot_elems, p[1].a.nslots * p[1].a.slot_elems);
   return true;
+}
+
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+static EncodeTiledFn encoder() {
+  static EncodeTiledFn fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = (EncodeTiledFn)p;
+  }
+  return fn;
+}
+
+int encode_input(Pass& p, const void* src) {
+  EncodeTiledFn enc = encoder();
+  if (!enc) return 1;
+  Args& a = p.a;
+  const int64_t RB = p.rb;
+  cuuint64_t dims[3] = {(cuuint64_t)a.LS, (cuuint64_t)RB, 256};
+  cuuint64_t strides[2] = {(cuuint64_t)(a.LS * 8), (cuuint64_t)(RB * a.LS * 8)};
+  cuuint32_t box[3] = {16, 1, 256};
+  cuuint32_t es[3] = {1, 1, 1};
+  CUresult r = enc(&a.mapA, CU_TENSOR_MAP_DATA_TYPE_UINT64, 3, const_cast<void*>(src), dims, strides, box, es,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return (int)r;
+  p.mapA_ptr = src;
+  return 0;
+}
+
+int encode_ring(Pass& p, void* staging) {
+  EncodeTiledFn enc = encoder();
+  if (!enc) return 1;
+  Args& a = p.a;
+  const int64_t RB = p.rb, DB = 256 / RB;
+  // T1 ring [j2l 16][ja RB][ks 16][kt 16] per slot
+  cuuint64_t dims[5] = {16, 16, (cuuint64_t)RB, 16, (cuuint64_t)a.nslots};
+  cuuint64_t strides[4] = {16 * 8, 256 * 8, (cuuint64_t)(RB * 256 * 8), (cuuint64_t)(16 * RB * 256 * 8)};
+  cuuint32_t box[5] = {16, 1, (cuuint32_t)RB, (cuuint32_t)DB, 1};
+  cuuint32_t es[5] = {1, 1, 1, 1, 1};
+  CUresult r = enc(&a.mapB, CU_TENSOR_MAP_DATA_TYPE_UINT64, 5, staging, dims, strides, box, es,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? 0 : (int)r;
 }
 
 }  // namespace lean

@@ -13,6 +13,7 @@
 // sub-stage B (rho_b-point DFTs, ring -> HBM); 32 KB tiles, 16 elements per
 // thread, four CTAs per SM.
 #pragma once
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <stddef.h>
 #include <stdint.h>
@@ -21,6 +22,8 @@ namespace efft {
 namespace lean {
 
 struct Args {
+  CUtensorMap mapA;    // prefetching pair kernel: the pass input, box {16, 1, 256}, 128B swizzle
+  CUtensorMap mapB;    // prefetching pair kernel, transposing pass: the staging ring
   const void* src;
   void* dst;
   void* stg;
@@ -50,6 +53,8 @@ struct Pass {
   int grid, nt, smem;
   int ra, rb;
   bool wide = false;  // 32-column groups (lean_wide)
+  bool pf = false;    // prefetching pair kernel (TMA landing buffer)
+  const void* mapA_ptr = nullptr;
   int64_t counter_ints;  // 2 (task counter) + 2 * ngroups
 };
 
@@ -64,6 +69,9 @@ bool plan(int64_t n, int c128, int inverse, bool scale_inverse, bool check_finit
 //           W_N^((q L2 + c) k1) fused into the transposing store;
 //   pass 2: T_q[n2][k1'] (N2 x L1) -> X_q[k2][k1'] in place (inverse: 1/N).
 bool split_sharded(int64_t n, int G, int c128, int64_t* N1, int64_t* N2);
+// prefetching pair kernel: (re-)encode the input map for src; encode the ring map (T1); 0 = ok
+int encode_input(Pass& p, const void* src);
+int encode_ring(Pass& p, void* staging);
 bool plan_sharded(int64_t n, int G, int rank, int c128, int inverse, bool check_finite, int num_sms, Pass p[2],
                   int64_t* staging_elems, int* err_cuda, bool blocked = false);
 
