@@ -340,16 +340,20 @@ def run_transform(handle: TransformHandle) -> np.ndarray:
 
 
 class PermSpectrum:
-    """A length-M packed real spectrum [R_0, R_{M/2}, R_1, I_1, ...] (reference core.py:199-249)."""
+    """View of a real-input spectrum in the packed layout of the reference
+    (core.py:10-15, contract of core.py:199-249): slot 0 = F_0, slot 1 = F_{M/2},
+    slots 2k, 2k+1 = Re, Im of F_k for 0 < k < M/2; the upper half follows from
+    F_{M-k} = conj(F_k)."""
 
     def __init__(self, packed: np.ndarray):
-        packed = np.asarray(packed)
-        if packed.ndim != 1 or packed.shape[0] < 2 or packed.shape[0] % 2 != 0:
+        buf = np.asarray(packed)
+        m = buf.shape[0] if buf.ndim == 1 else 0
+        if m < 2 or m & 1:
             raise ValueError("packed spectrum must be 1-D with even length >= 2")
-        self.packed = packed
+        self.packed = buf
 
     def __len__(self) -> int:
-        return self.packed.shape[0]
+        return len(self.packed)
 
     @property
     def dc(self) -> float:
@@ -360,33 +364,31 @@ class PermSpectrum:
         return float(self.packed[1])
 
     def coefficient(self, k: int) -> complex:
-        m = self.packed.shape[0]
-        if not 0 <= k < m:
+        """F_k for any 0 <= k < M."""
+        m = len(self.packed)
+        if k < 0 or k >= m:
             raise IndexOutOfRange(f"coefficient index {k} outside [0, {m})")
-        if k == 0:
-            return complex(self.packed[0])
-        if k == m // 2:
-            return complex(self.packed[1])
-        if k > m // 2:
-            return self.coefficient(m - k).conjugate()
-        return complex(float(self.packed[2 * k]), float(self.packed[2 * k + 1]))
+        h = m // 2
+        mirrored = k > h
+        j = m - k if mirrored else k
+        if j == 0:
+            val = complex(self.packed[0])
+        elif j == h:
+            val = complex(self.packed[1])
+        else:
+            val = complex(float(self.packed[2 * j]), float(self.packed[2 * j + 1]))
+        return val.conjugate() if mirrored else val
 
     def to_complex(self) -> np.ndarray:
-        m = self.packed.shape[0]
-        out = np.empty(m // 2 + 1, dtype=np.complex128)
-        out[0] = self.packed[0]
-        out[-1] = self.packed[1]
-        out.real[1:-1] = self.packed[2::2]
-        out.imag[1:-1] = self.packed[3::2]
-        return out
+        """F_0 .. F_{M/2} as complex128."""
+        p = np.asarray(self.packed, dtype=np.float64)
+        inner = p[2:].reshape(-1, 2)
+        return np.concatenate(([p[0]], inner[:, 0] + 1j * inner[:, 1], [p[1]])).astype(np.complex128)
 
     def to_full_complex(self) -> np.ndarray:
-        half = self.to_complex()
-        m = self.packed.shape[0]
-        out = np.empty(m, dtype=np.complex128)
-        out[: m // 2 + 1] = half
-        out[m // 2 + 1:] = np.conj(half[-2:0:-1])
-        return out
+        """All M coefficients, the upper half by conjugate symmetry."""
+        lower = self.to_complex()
+        return np.concatenate((lower, np.conj(lower[1:-1][::-1])))
 
 
 def pack_perm(coeffs) -> np.ndarray:

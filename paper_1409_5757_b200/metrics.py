@@ -22,11 +22,12 @@ def flops_model(n: int, complex_input: bool = False) -> float:
 
 
 def efficiency(perf_by_workers: dict) -> dict:
-    """Parallel efficiency eta(T) = P(T) / (T * P(1)) (reference bench.py:34-39)."""
-    if 1 not in perf_by_workers or not perf_by_workers[1] > 0:
+    """Parallel efficiency P(T) / (T * P(1)) per worker count T (the reference's
+    definition, bench.py:34-39; on the GPU the worker count has no effect)."""
+    base = perf_by_workers.get(1)
+    if base is None or not base > 0:
         raise MissingBaseline("need a positive single-worker performance P(1)")
-    p1 = perf_by_workers[1]
-    return {t: p / (t * p1) for t, p in perf_by_workers.items()}
+    return {workers: perf / (workers * base) for workers, perf in perf_by_workers.items()}
 
 
 def algorithmic_bytes(n: int, elem_bytes: int, passes: int) -> int:
