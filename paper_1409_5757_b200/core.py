@@ -178,6 +178,7 @@ class TransformHandle:
         self._native = _native.NativePlan(plan.n, native_dtype, plan.direction, plan.device,
                                           _native.EFFT_FLAG_CHECK_FINITE)
         self._dev_in = self._dev_out = None
+        self._host_in = self._host_out = None
         self._data = self._result = None
         self._closed = False
 

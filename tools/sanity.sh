@@ -1,0 +1,9 @@
+#!/bin/bash
+# GPU-box sanity check (dev tool): smoke, gpu tests, the C3 bench line.
+set -u
+mkdir -p gpurun_out
+timeout 600 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke rc=$?" >> gpurun_out/smoke.log
+timeout 2400 python -m pytest tests -m gpu -x -q -rs > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
+timeout 900 python bench.py --steps 20 --warmup 3 > gpurun_out/bench_c3.log 2>&1; echo "bench rc=$?"
+tail -n 3 gpurun_out/smoke.log
+tail -n 5 gpurun_out/pytest_gpu.log
