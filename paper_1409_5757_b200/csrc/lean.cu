@@ -379,8 +379,10 @@ __global__ void __launch_bounds__(LT<R>::NT, MINB) lean_pass(const __grid_consta
         for (int t = 0; t < A0; ++t) nf |= !(isfinite(v[t].x) && isfinite(v[t].y));
       }
       if constexpr (T1) {
+        if (a.cin.y != 1.0) {  // inverse: conjugate the input (forward: identity)
 #pragma unroll
-        for (int t = 0; t < A0; ++t) v[t] = cscale(v[t], cvt(a.cin, R()));
+          for (int t = 0; t < A0; ++t) v[t] = cscale(v[t], cvt(a.cin, R()));
+        }
       }
       reg_dft<R, A0>(v);
       {
@@ -430,8 +432,13 @@ __global__ void __launch_bounds__(LT<R>::NT, MINB) lean_pass(const __grid_consta
         const int kb = task * DB + dl;
         V* op = DST + (int64_t)g * F + lane + a.LS * (int64_t)(kb + RA * kq);
         const int64_t step = a.LS * (int64_t)(RA * QB);
+        if (a.cout.x == 1.0 && a.cout.y == 1.0) {  // forward: no conjugation, no scale
 #pragma unroll
-        for (int kp = 0; kp < 16; ++kp) st_hint(op + kp * step, cscale(v[P<16>(kp)], cvt(a.cout, R())), pol);
+          for (int kp = 0; kp < 16; ++kp) st_hint(op + kp * step, v[P<16>(kp)], pol);
+        } else {
+#pragma unroll
+          for (int kp = 0; kp < 16; ++kp) st_hint(op + kp * step, cscale(v[P<16>(kp)], cvt(a.cout, R())), pol);
+        }
       }
     } else if (T1 || r < A0) {
       // ---- sub-stage A, stage 1: A1-point DFT over s -> ks, store to the ring
@@ -675,11 +682,13 @@ __global__ void __launch_bounds__(pair::NT, PF ? 3 : 4) lean_pair(const __grid_c
           nf |= !(isfinite(x[t].x) && isfinite(x[t].y) && isfinite(y[t].x) && isfinite(y[t].y));
       }
       if constexpr (T1) {
-        const V ci = cvt(a.cin, 0.f);
+        if (a.cin.y != 1.0) {  // inverse: conjugate the input (forward: identity)
+          const V ci = cvt(a.cin, 0.f);
 #pragma unroll
-        for (int t = 0; t < 16; ++t) {
-          x[t] = mul2(x[t], ci);
-          y[t] = mul2(y[t], ci);
+          for (int t = 0; t < 16; ++t) {
+            x[t] = mul2(x[t], ci);
+            y[t] = mul2(y[t], ci);
+          }
         }
       }
       reg_dft<float, 16>(x);
@@ -753,8 +762,14 @@ __global__ void __launch_bounds__(pair::NT, PF ? 3 : 4) lean_pair(const __grid_c
         const V co = cvt(a.cout, 0.f);
         V* op = DST + (int64_t)g * 16 + 2 * cp + a.LS * (int64_t)(kb + 256 * kq);
         const int64_t step = a.LS * (int64_t)(256 * QB);
+        if (a.cout.x == 1.0 && a.cout.y == 1.0) {  // forward: no conjugation, no scale
 #pragma unroll
-        for (int kp = 0; kp < 16; ++kp) pair::st16(op + kp * step, mul2(x[P<16>(kp)], co), mul2(y[P<16>(kp)], co), pol);
+          for (int kp = 0; kp < 16; ++kp) pair::st16(op + kp * step, x[P<16>(kp)], y[P<16>(kp)], pol);
+        } else {
+#pragma unroll
+          for (int kp = 0; kp < 16; ++kp)
+            pair::st16(op + kp * step, mul2(x[P<16>(kp)], co), mul2(y[P<16>(kp)], co), pol);
+        }
       }
     } else {
       // ---- A stage 1: 16-point DFTs over s -> ks, store to the ring
@@ -782,6 +797,500 @@ __global__ void __launch_bounds__(pair::NT, PF ? 3 : 4) lean_pair(const __grid_c
     sc.end(a, isB, g);
   }
   sc.finish(a, nf);
+#undef SRC
+#undef DST
+#undef STG
+}
+
+// Pipelined complex64 tile kernel (EFFT_LEAN_PIPE): the paired kernel's tile
+// arithmetic (32 points per thread, 128 threads per 32 KB tile) fed by TMA.
+// One CTA per SM, 16 warps (all the register file holds at 128 registers):
+//   * warps 0-11: three independent compute groups of 128 threads; group q owns
+//     two 32 KB buffers: tile k + 1 lands in one while tile k is computed in the
+//     other.  A group waits on the buffer's `full` mbarrier, reads its stage-0
+//     points from it (A tiles: 128-byte-swizzled rows), uses the SAME buffer
+//     for the exchange between the two radix stages (the transposing exchange
+//     of the T1 A tile is XOR-swizzled, [s][kt][j2 pair ^ (kt >> 1)], so it
+//     fits 32 KB without padding, both sides conflict-free), arrives on `empty`
+//     once its stage-1 operands are in registers, stores from registers and
+//     arrives on `done`.  Two 128-thread named barriers per tile; no CTA-wide
+//     barrier, no fence, no atomic and no dependency probe in a compute warp.
+//   * warps 12-14, lane 0: issue lanes, one per group (a blocked dependency
+//     probe of one never delays another).  Static schedule: group
+//     q of CTA c runs positions v, v + 3G, v + 6G, ... of the claim order
+//     (v = c + q G, G = grid; all CTAs resident), so only the tiles in the
+//     buffers are in flight and the staging ring stays L2-resident (a claim
+//     counter running ahead widens the window of open groups).  A lane probes
+//     the next position's dependency counter (ld.acquire) one tile ahead and
+//     issues the tile with ONE TMA instruction the moment its buffer is free.
+//   * warp 15, lane 0: the release lane: `done` seen (any group) -> ONE
+//     fence.acq_rel (the tiles' stores, observed through the mbarriers, become
+//     visible GPU-wide) -> a red per tile on its group's completion counter.
+//     Its fence never delays an issue.  Nothing in either loop blocks, positions increase per group and
+//     every dependency points backwards: the header's deadlock-freedom argument
+//     holds unchanged.
+namespace pipe {
+constexpr int NG = 3;                 // compute groups
+constexpr int NC = 128;               // threads per group
+constexpr int NT = NG * NC + 128;     // + three issue warps (one lane each) and the release warp
+constexpr int BUF = 32768;
+struct Desc {
+  int isB, g, task, pad;
+  long long t_issue;  // dev profiling (EFFT_PIPE_ABL bit 256)
+};
+struct Group {
+  uint64_t full[2], empty[2], done[4];  // done: a ring of 4 so an unobserved phase is never overrun
+  Desc desc[2];
+  int32_t* pend[4];                 // issue lane -> release lane: the completion counter of tile k (k & 3)
+  volatile int ntiles;              // issue lane -> release lane: tiles issued in all (-1 while running)
+  volatile uint32_t released;       // release lane -> issue lane: tiles published
+  long long t_empty[2], t_done[4];  // dev profiling
+};
+struct Shared {
+  Group grp[NG];
+};
+constexpr int SMEM = 2 * NG * BUF + 512 * 8 + (int)sizeof(Shared);
+__device__ __forceinline__ void bar_compute(int q) { asm volatile("bar.sync %0, 128;" ::"r"(q + 1) : "memory"); }
+}  // namespace pipe
+
+// dev ablations (EFFT_PIPE_ABL bits, timing only -- results are wrong): 1 no arithmetic,
+// 2 no global stores (32 / 64: no ring / no output stores), 4 no exchange, 8 no TMA loads,
+// 16 no four-step twiddle, 256 cycle counters, 512 no dependencies, 1024 no release fence
+#define ABL(bit) ((a.abl & (bit)) != 0)
+template <int RB, bool T1>
+__global__ void __launch_bounds__(pipe::NT, 1) lean_pipe(const __grid_constant__ Args a) {
+  using V = float2;
+  constexpr int QB = RB / 16, DB = 16 / QB;
+  extern __shared__ __align__(1024) unsigned char smraw[];
+  V* w256 = reinterpret_cast<V*>(smraw + 2 * pipe::NG * pipe::BUF);
+  V* wlo = w256 + 256;
+  pipe::Shared* shs = reinterpret_cast<pipe::Shared*>(wlo + 256);
+#define SRC reinterpret_cast<const V*>(a.src)
+#define DST reinterpret_cast<V*>(a.dst)
+#define STG reinterpret_cast<V*>(a.stg)
+  for (int i = threadIdx.x; i < 256; i += pipe::NT) {
+    w256[i] = to_v(wroot(i, 256), 0.f);
+    wlo[i] = to_v(wroot(i, a.R), 0.f);
+  }
+  if (threadIdx.x < pipe::NG) {
+    pipe::Group* sh = &shs->grp[threadIdx.x];
+    sh->ntiles = -1;
+    sh->released = 0;
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&sh->full[i], 1);
+      mbar_init(&sh->empty[i], pipe::NC);
+    }
+    for (int i = 0; i < 4; ++i) mbar_init(&sh->done[i], pipe::NC);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (threadIdx.x >= pipe::NG * pipe::NC + 96) {
+    // ---------------- release lane ----------------
+    // One lane for the three groups: every `done` seen in a sweep is published
+    // behind ONE fence.acq_rel (the tiles' stores, observed through the
+    // mbarriers, become visible GPU-wide), then one red per tile on its group's
+    // completion counter.  `released` tells the issue lanes how far it got, so
+    // the `done` / pend rings are never overrun.
+    if (threadIdx.x != pipe::NG * pipe::NC + 96) return;
+    uint32_t kr[pipe::NG] = {0, 0, 0}, kn[pipe::NG];
+    long long idle = 0;
+    for (;;) {
+      bool any = false, fin = true;
+#pragma unroll
+      for (int q = 0; q < pipe::NG; ++q) {
+        pipe::Group* sh = &shs->grp[q];
+        kn[q] = kr[q];
+        while (kn[q] - kr[q] < 3 && mbar_test(&sh->done[kn[q] & 3], (kn[q] >> 2) & 1)) ++kn[q];
+        any |= kn[q] != kr[q];
+        const int nt = sh->ntiles;
+        fin &= nt >= 0 && kn[q] == (uint32_t)nt;
+      }
+      if (any) {
+        if (!ABL(1024)) asm volatile("fence.acq_rel.gpu;" ::: "memory");
+#pragma unroll
+        for (int q = 0; q < pipe::NG; ++q) {
+          pipe::Group* sh = &shs->grp[q];
+          for (; kr[q] != kn[q]; ++kr[q])
+            asm volatile("red.relaxed.gpu.global.add.s32 [%0], 1;" ::"l"(sh->pend[kr[q] & 3]) : "memory");
+          sh->released = kr[q];
+        }
+        idle = 0;
+      } else if (fin) {
+        break;
+      } else {
+        __nanosleep(64);
+        if (++idle == (1ll << 24)) {
+          printf("EFFT lean pipe release lane stuck cta=%d kr=%u %u %u\n", blockIdx.x, kr[0], kr[1], kr[2]);
+          __trap();
+        }
+      }
+    }
+    return;
+  }
+  if (threadIdx.x >= pipe::NG * pipe::NC) {
+    // ---------------- issue lanes (lane 0 of warps 12, 13, 14) ----------------
+    if (threadIdx.x % 32 != 0) return;
+    const int q = (threadIdx.x - pipe::NG * pipe::NC) / 32;
+    pipe::Group* sh = &shs->grp[q];
+    unsigned char* const bufs = smraw + q * 2 * pipe::BUF;
+    const uint64_t pol = policy_evict_first();
+    struct Task {
+      long long pos;
+      int isB, g, task, val, need;
+    };
+    auto probe = [&](const Task& t) -> int {
+      if (t.isB) return ld_acquire(a.doneA + t.g);        // B(g) needs A(g) complete
+      if (t.g < a.nslots) return a.ntB;
+      return ld_acquire(a.doneB + (t.g - a.nslots));      // A(g) stores into the slot B(g - nslots) read
+    };
+    auto setup = [&](Task& t, long long pos) {
+      t.pos = pos;
+      t.isB = t.g = t.task = 0;
+      t.val = t.need = 0;
+      if (pos < a.total) {
+        decode(a, (uint32_t)pos, t.isB, t.g, t.task);
+        t.need = t.isB ? a.ntA : a.ntB;
+        t.val = probe(t);
+      }
+    };
+    const long long G = (long long)gridDim.x * pipe::NG, v = blockIdx.x + (long long)q * gridDim.x;
+    Task cur, nxt;
+    setup(cur, v);
+    setup(nxt, v + G);
+    uint32_t ki = 0, ke = 0;  // tiles issued / buffer freed
+    long long idle = 0, late = 0, obs_e = 0, iss_d = 0, t_obs[2] = {0, 0};
+    for (;;) {
+      bool prog = false;
+      while (ke < ki && mbar_test(&sh->empty[ke & 1], (ke >> 1) & 1)) {
+        if (ABL(256)) {
+          t_obs[ke & 1] = clock64();
+          obs_e += t_obs[ke & 1] - sh->t_empty[ke & 1];
+        }
+        ++ke;
+        prog = true;
+      }
+      // (ki - released < 4: the `done` ring and the pend ring are never overrun)
+      if (ki - ke < 2 && ki - sh->released < 4) {
+        const int b = ki & 1;
+        if (cur.pos >= a.total) {
+          sh->desc[b].isB = -1;
+          mbar_arrive(&sh->full[b]);
+          sh->ntiles = (int)ki;
+          if (ABL(256) && blockIdx.x < 2)
+            printf("pipe prof cta %d group %d issue lane: tiles %u, late deps %lld, empty arrive->seen %lld, "
+                   "seen->issue %lld\n", blockIdx.x, q, ki, late, obs_e / (ki ? ki : 1), iss_d / (ki ? ki : 1));
+          break;
+        }
+        if (ABL(512)) cur.val = cur.need;
+        if (cur.val < cur.need) {  // the producers of this tile are late
+          cur.val = probe(cur);
+          ++late;
+        }
+        if (cur.val >= cur.need) {
+          sh->desc[b].isB = cur.isB;
+          sh->desc[b].g = cur.g;
+          sh->desc[b].task = cur.task;
+          sh->pend[ki & 3] = cur.isB ? a.doneB + cur.g : a.doneA + cur.g;
+          if (ABL(256)) {
+            sh->desc[b].t_issue = clock64();
+            if (ki >= 2) iss_d += sh->desc[b].t_issue - t_obs[b];
+          }
+          unsigned char* land = bufs + b * pipe::BUF;
+          asm volatile("fence.proxy.async.global;" ::: "memory");
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          if (ABL(8)) {
+            mbar_arrive(&sh->full[b]);
+          } else {
+            mbar_arrive_tx(&sh->full[b], pipe::BUF);
+            if (!cur.isB) {
+              tma_load_3d(land, &a.mapA, cur.g * 16, cur.task, 0, &sh->full[b], pol);
+            } else if constexpr (T1) {
+              tma_load_5d(land, &a.mapB, 0, cur.task & 15, 0, (cur.task >> 4) * DB, cur.g % a.nslots, &sh->full[b],
+                          pol);
+            } else {
+              const V* src = STG + (int64_t)(cur.g % a.nslots) * a.slot_elems + (int64_t)(cur.task * DB) * RB * 16;
+              bulk_g2s(land, src, pipe::BUF, &sh->full[b], pol);
+            }
+          }
+          ++ki;
+          cur = nxt;
+          setup(nxt, v + (long long)(ki + 1) * G);
+          prog = true;
+        }
+      }
+      if (!prog) {
+        __nanosleep(a.abl >> 16 ? (a.abl >> 16) : 64);
+        if (++idle == (1ll << 24)) {
+          printf("EFFT lean pipe issue lane stuck cta=%d q=%d pos=%lld isB=%d g=%d task=%d ki=%u ke=%u released=%u\n",
+                 blockIdx.x, q, cur.pos, cur.isB, cur.g, cur.task, ki, ke, sh->released);
+          __trap();
+        }
+      } else {
+        idle = 0;
+      }
+    }
+    return;
+  }
+  // ---------------- compute warps ----------------
+  const int q = threadIdx.x / pipe::NC, tid = threadIdx.x % pipe::NC;
+  pipe::Group* sh = &shs->grp[q];
+  unsigned char* const bufs = smraw + q * 2 * pipe::BUF;
+  const int cp = tid % 8, r = tid / 8;
+  bool nf = false;
+  long long pw = 0, pl = 0, pt0 = clock64(), pn = 0;  // dev profiling
+  for (uint32_t k = 0;; ++k) {
+    const int b = k & 1;
+    const long long tw = ABL(256) ? clock64() : 0;
+    mbar_wait(&sh->full[b], (k >> 1) & 1);
+    const int isB = sh->desc[b].isB;
+    if (isB < 0) break;
+    if (ABL(256)) {
+      const long long tn = clock64();
+      pw += tn - tw;
+      pl += tn - sh->desc[b].t_issue;
+      ++pn;
+    }
+    const int g = sh->desc[b].g, task = sh->desc[b].task;
+    V* sp = STG + (int64_t)(g % a.nslots) * a.slot_elems;
+    unsigned char* const buf = bufs + b * pipe::BUF;
+    V* xb = reinterpret_cast<V*>(buf);
+    float4* xq = reinterpret_cast<float4*>(buf);
+    V x[16], y[16];  // columns 2cp (x) and 2cp + 1 (y)
+    if (isB) {  // [dl][ja][16 lanes] rows of 128 bytes
+#pragma unroll
+      for (int dl = 0; dl < DB; ++dl)
+#pragma unroll
+        for (int q = 0; q < QB; ++q) {
+          const float4 t = xq[(dl * RB + r + 16 * q) * 8 + cp];
+          x[dl * QB + q] = make_float2(t.x, t.y);
+          y[dl * QB + q] = make_float2(t.z, t.w);
+        }
+    } else {  // [jb][16 columns], 16-byte chunk c of row jb at c ^ (jb & 7); jb = r + 16 t
+      const float4* L = xq + r * 8 + (cp ^ (r & 7));
+#pragma unroll
+      for (int t = 0; t < 16; ++t) {
+        const float4 u = L[t * 128];
+        x[t] = make_float2(u.x, u.y);
+        y[t] = make_float2(u.z, u.w);
+      }
+    }
+    if (!ABL(4)) pipe::bar_compute(q);  // every thread has its points: the buffer becomes the exchange
+    if (ABL(1)) {
+    } else if (isB) {
+      // ---- B stage 0: W_R^(ja kb), QB-point DFTs
+#pragma unroll
+      for (int dl = 0; dl < DB; ++dl) {
+        const int kb = T1 ? 2 * cp + 16 * (task & 15) : task * DB + dl;
+        const int e0 = r * kb, es = 16 * kb;  // < R
+        V w = cmul(w256[(e0 >> 8) * (256 / RB)], wlo[e0 & 255]);
+        const V st = cmul(w256[(es >> 8) * (256 / RB)], wlo[es & 255]);
+        if constexpr (T1) {
+          const int e1 = e0 + r, es1 = es + 16;  // kb + 1
+          V w1 = cmul(w256[(e1 >> 8) * (256 / RB)], wlo[e1 & 255]);
+          const V st1 = cmul(w256[(es1 >> 8) * (256 / RB)], wlo[es1 & 255]);
+#pragma unroll
+          for (int q = 0; q < QB; ++q) {
+            x[dl * QB + q] = cmul(x[dl * QB + q], w);
+            y[dl * QB + q] = cmul(y[dl * QB + q], w1);
+            if (q + 1 < QB) {
+              w = cmul(w, st);
+              w1 = cmul(w1, st1);
+            }
+          }
+        } else {
+#pragma unroll
+          for (int q = 0; q < QB; ++q) {
+            x[dl * QB + q] = cmul(x[dl * QB + q], w);
+            y[dl * QB + q] = cmul(y[dl * QB + q], w);
+            if (q + 1 < QB) w = cmul(w, st);
+          }
+        }
+      }
+#pragma unroll
+      for (int dl = 0; dl < DB; ++dl) {
+        reg_dft<float, QB>(x + dl * QB);
+        reg_dft<float, QB>(y + dl * QB);
+      }
+      {  // W_RB^(p kq)
+        const V* wp = w256;
+#pragma unroll
+        for (int k2 = 1; k2 < QB; ++k2) {
+          wp += r * (256 / RB);
+          const V w = *wp;
+#pragma unroll
+          for (int dl = 0; dl < DB; ++dl) {
+            x[dl * QB + P<QB>(k2)] = cmul(x[dl * QB + P<QB>(k2)], w);
+            y[dl * QB + P<QB>(k2)] = cmul(y[dl * QB + P<QB>(k2)], w);
+          }
+        }
+      }
+    } else {
+      // ---- A stage 0: 16-point DFTs over t, W_256^(s kt) shared by the pair
+      if (a.check_finite) {
+#pragma unroll
+        for (int t = 0; t < 16; ++t)
+          nf |= !(isfinite(x[t].x) && isfinite(x[t].y) && isfinite(y[t].x) && isfinite(y[t].y));
+      }
+      if constexpr (T1) {
+        if (a.cin.y != 1.0) {  // inverse: conjugate the input (forward: identity)
+          const V ci = cvt(a.cin, 0.f);
+#pragma unroll
+          for (int t = 0; t < 16; ++t) {
+            x[t] = mul2(x[t], ci);
+            y[t] = mul2(y[t], ci);
+          }
+        }
+      }
+      reg_dft<float, 16>(x);
+      reg_dft<float, 16>(y);
+      {
+        const V* wp = w256;
+#pragma unroll
+        for (int k2 = 1; k2 < 16; ++k2) {
+          wp += r;
+          const V w = *wp;
+          x[P<16>(k2)] = cmul(x[P<16>(k2)], w);
+          y[P<16>(k2)] = cmul(y[P<16>(k2)], w);
+        }
+      }
+    }
+    if (ABL(4)) {
+    } else if (isB) {
+      // the consumed staging lines leave L2 without write-back
+#pragma unroll
+      for (int i = cp; i < 16; i += 8) l2_discard(sp + pair_b_line<RB, T1>(task, i / QB, r, i % QB));
+#pragma unroll
+      for (int dl = 0; dl < DB; ++dl)
+#pragma unroll
+        for (int k2 = 0; k2 < QB; ++k2) {
+          const V u = x[dl * QB + P<QB>(k2)], w = y[dl * QB + P<QB>(k2)];
+          xq[((dl * QB + k2) * 16 + r) * 8 + cp] = make_float4(u.x, u.y, w.x, w.y);
+        }
+    } else {
+#pragma unroll
+      for (int k2 = 0; k2 < 16; ++k2) {
+        const V u = x[P<16>(k2)], w = y[P<16>(k2)];
+        if constexpr (T1)  // [s][kt][j2 pair ^ (kt >> 1)]
+          xq[r * 128 + k2 * 8 + (cp ^ (k2 >> 1))] = make_float4(u.x, u.y, w.x, w.y);
+        else  // [kt][s][pair]
+          xq[(k2 * 16 + r) * 8 + cp] = make_float4(u.x, u.y, w.x, w.y);
+      }
+    }
+    if (!ABL(4)) pipe::bar_compute(q);
+    if (isB) {
+      // ---- B stage 1: 16-point DFTs over p; thread (cp, dl, kq)
+      const int kq = r % QB, dl = r / QB;
+      if (!ABL(4)) {
+#pragma unroll
+      for (int u = 0; u < 16; ++u) {
+        const float4 t = xq[((dl * QB + kq) * 16 + u) * 8 + cp];
+        x[u] = make_float2(t.x, t.y);
+        y[u] = make_float2(t.z, t.w);
+      }
+      }
+      if (ABL(256) && tid == 0) sh->t_empty[b] = clock64();
+      mbar_arrive(&sh->empty[b]);  // stage-1 operands are in registers: the buffer is free
+      if (!ABL(1)) {
+      reg_dft<float, 16>(x);
+      reg_dft<float, 16>(y);
+      }
+      const uint64_t pol = policy_evict_first();
+      if constexpr (T1) {
+        // y[k1 + R1 j2] = Y W_N^(j2 k1), k1 = kt + 16 ks + 256 kq + 256 QB kp, kt = 2cp (+1)
+        const int j2 = g * 16 + (task >> 4) * DB + dl;
+        const uint32_t c = (uint32_t)(2 * cp + 16 * (task & 15) + 256 * kq);
+        // exact integer exponents, fp64 bases and step, fp64 recurrence (see lean_pair)
+        const uint64_t N = (uint64_t)a.N, jg = (uint64_t)(a.j2off + j2);
+        double2 w0 = wroot((int64_t)((jg * c) % N), a.N);
+        const V wj = to_v(wroot((int64_t)(jg % N), a.N), 0.f);
+        const double2 st = wroot((int64_t)((jg * (256 * QB)) % N), a.N);
+        if (ABL(2) || ABL(64)) {
+        } else if (ABL(128)) {  // timing experiment: the same bytes as 256-byte segments
+          const int ks = task & 15;
+          V* op = DST + (int64_t)(g * 16 + (task >> 4) * DB + (ks & 1)) * a.R + 2 * cp + 16 * (r & 1) + 32 * (ks >> 1) +
+                  256 * ((r >> 1) & (QB - 1));
+#pragma unroll
+          for (int kp = 0; kp < 16; ++kp) pair::st16(op + kp * (256 * QB), x[P<16>(kp)], y[P<16>(kp)], pol);
+        } else if (ABL(16)) {
+          V* op = DST + (int64_t)j2 * a.R + c;
+#pragma unroll
+          for (int kp = 0; kp < 16; ++kp) pair::st16(op + kp * (256 * QB), x[P<16>(kp)], y[P<16>(kp)], pol);
+        } else if (a.obl == 0) {
+          V* op = DST + (int64_t)j2 * a.R + c;
+#pragma unroll
+          for (int kp = 0; kp < 16; ++kp) {
+            const V w = to_v(w0, 0.f);
+            pair::st16(op + kp * (256 * QB), cmul(x[P<16>(kp)], w), cmul(y[P<16>(kp)], cmul(w, wj)), pol);
+            if (kp < 15) w0 = cmul(w0, st);
+          }
+        } else {
+#pragma unroll
+          for (int kp = 0; kp < 16; ++kp) {
+            const V w = to_v(w0, 0.f);
+            pair::st16(DST + t1_out(a, j2, c + kp * (256 * QB)), cmul(x[P<16>(kp)], w),
+                       cmul(y[P<16>(kp)], cmul(w, wj)), pol);
+            if (kp < 15) w0 = cmul(w0, st);
+          }
+        }
+      } else {
+        const int kb = task * DB + dl;
+        const V co = cvt(a.cout, 0.f);
+        V* op = DST + (int64_t)g * 16 + 2 * cp + a.LS * (int64_t)(kb + 256 * kq);
+        if (ABL(128))  // timing experiment: the same bytes as 256-byte segments
+          op = DST + (int64_t)(g >> 1) * 32 + 16 * (r & 1) + 2 * cp +
+               a.LS * (int64_t)(task * DB + (g & 1) + 256 * ((r >> 1) & (QB - 1)));
+        const int64_t step = a.LS * (int64_t)(256 * QB);
+        if (ABL(2) || ABL(64)) {
+        } else if (a.cout.x == 1.0 && a.cout.y == 1.0) {  // forward: no conjugation, no scale
+#pragma unroll
+          for (int kp = 0; kp < 16; ++kp) pair::st16(op + kp * step, x[P<16>(kp)], y[P<16>(kp)], pol);
+        } else {
+#pragma unroll
+          for (int kp = 0; kp < 16; ++kp)
+            pair::st16(op + kp * step, mul2(x[P<16>(kp)], co), mul2(y[P<16>(kp)], co), pol);
+        }
+      }
+    } else {
+      // ---- A stage 1: 16-point DFTs over s -> ks, store to the ring
+      // T0 thread (pair cp, kt = r): ring [kb][ja][lane], kb = kt + 16 ks
+      // T1 thread (kt pair cp, j2l = r): ring [j2l][ja][ks][kt]
+      if (ABL(4)) {
+      } else if constexpr (T1) {
+        const V* L = xb + (2 * cp) * 16 + (((r >> 1) ^ cp) & 7) * 2 + (r & 1);
+#pragma unroll
+        for (int u = 0; u < 16; ++u) {
+          x[u] = L[u * 256];
+          y[u] = L[u * 256 + 16];
+        }
+      } else {
+#pragma unroll
+        for (int u = 0; u < 16; ++u) {
+          const float4 t = xq[(r * 16 + u) * 8 + cp];
+          x[u] = make_float2(t.x, t.y);
+          y[u] = make_float2(t.z, t.w);
+        }
+      }
+      if (ABL(256) && tid == 0) sh->t_empty[b] = clock64();
+      mbar_arrive(&sh->empty[b]);
+      if (!ABL(1)) {
+      reg_dft<float, 16>(x);
+      reg_dft<float, 16>(y);
+      }
+      const int base = T1 ? (r * RB + task) * 256 + 2 * cp : (r * RB + task) * 16 + 2 * cp;
+      const int step = T1 ? 16 : 16 * RB * 16;
+      const uint64_t keep = policy_evict_last();
+      if (!ABL(2) && !ABL(32)) {
+#pragma unroll
+      for (int ks = 0; ks < 16; ++ks) pair::st16(sp + base + ks * step, x[P<16>(ks)], y[P<16>(ks)], keep);
+      }
+    }
+    if (ABL(256) && tid == 0) sh->t_done[k & 3] = clock64();
+    mbar_arrive(&sh->done[k & 3]);  // stores issued
+  }
+  if (ABL(256) && tid == 0 && blockIdx.x < 2 && pn)
+    printf("pipe prof cta %d compute: %lld tiles, %lld cycles per tile, waiting for the tile %lld, issue->ready %lld\n",
+           blockIdx.x, pn, (clock64() - pt0) / pn, pw / pn, pl / pn);
+  if (__any_sync(0xffffffffu, nf) && (tid & 31) == 0) atomicOr(a.flag, 1);
 #undef SRC
 #undef DST
 #undef STG
@@ -956,11 +1465,13 @@ __global__ void __launch_bounds__(wide::NT, 2) lean_wide(const __grid_constant__
           nf |= !(isfinite(x[t].x) && isfinite(x[t].y) && isfinite(y[t].x) && isfinite(y[t].y));
       }
       if constexpr (T1) {
-        const V ci = cvt(a.cin, 0.f);
+        if (a.cin.y != 1.0) {  // inverse: conjugate the input (forward: identity)
+          const V ci = cvt(a.cin, 0.f);
 #pragma unroll
-        for (int t = 0; t < 16; ++t) {
-          x[t] = mul2(x[t], ci);
-          y[t] = mul2(y[t], ci);
+          for (int t = 0; t < 16; ++t) {
+            x[t] = mul2(x[t], ci);
+            y[t] = mul2(y[t], ci);
+          }
         }
       }
       reg_dft<float, 16>(x);
@@ -1031,8 +1542,14 @@ __global__ void __launch_bounds__(wide::NT, 2) lean_wide(const __grid_constant__
         const V co = cvt(a.cout, 0.f);
         V* op = DST + (int64_t)g * 32 + 2 * cp + a.LS * (int64_t)(kb + 256 * kq);
         const int64_t step = a.LS * (int64_t)(256 * QB);
+        if (a.cout.x == 1.0 && a.cout.y == 1.0) {  // forward: no conjugation, no scale
 #pragma unroll
-        for (int kp = 0; kp < 16; ++kp) pair::st16(op + kp * step, mul2(x[P<16>(kp)], co), mul2(y[P<16>(kp)], co), pol);
+          for (int kp = 0; kp < 16; ++kp) pair::st16(op + kp * step, x[P<16>(kp)], y[P<16>(kp)], pol);
+        } else {
+#pragma unroll
+          for (int kp = 0; kp < 16; ++kp)
+            pair::st16(op + kp * step, mul2(x[P<16>(kp)], co), mul2(y[P<16>(kp)], co), pol);
+        }
       }
     } else {
       // ---- A stage 1: 16-point DFTs over s -> ks, store to the ring
@@ -1123,6 +1640,22 @@ static bool use_pf(bool t1) {
   const int v = e ? atoi(e) : 0;
   return (v >> (t1 ? 0 : 1)) & 1;
 }
+static void* pick_pipe(int rb, bool t1) {
+  switch (rb) {
+    case 16: return t1 ? (void*)lean_pipe<16, true> : (void*)lean_pipe<16, false>;
+    case 32: return t1 ? (void*)lean_pipe<32, true> : (void*)lean_pipe<32, false>;
+    case 64: return t1 ? (void*)lean_pipe<64, true> : (void*)lean_pipe<64, false>;
+    case 128: return t1 ? (void*)lean_pipe<128, true> : (void*)lean_pipe<128, false>;
+    case 256: return t1 ? (void*)lean_pipe<256, true> : (void*)lean_pipe<256, false>;
+    default: return nullptr;
+  }
+}
+// EFFT_LEAN_PIPE: bit 0 = the pipelined kernel in the transposing pass, bit 1 = in the in-place pass
+static bool use_pipe(bool t1) {
+  const char* e = getenv("EFFT_LEAN_PIPE");
+  const int v = e ? atoi(e) : 0;
+  return (v >> (t1 ? 0 : 1)) & 1;
+}
 static void* pick_wide(int rb, bool t1) {
   switch (rb) {
     case 32: return t1 ? (void*)lean_wide<32, true> : (void*)lean_wide<32, false>;
@@ -1153,7 +1686,10 @@ static bool plan_pass(Pass& q, bool t1, int ra, int lb, int64_t cols, int64_t N,
                       bool allow_pf = true) {
   // complex64, RA = 256: the wide kernel (32-column groups, 256-byte segments)
   // when enabled and the columns divide, else the paired one (16 columns)
-  const bool wide = !c128 && ra == 256 && lb >= 5 && use_wide(t1) && cols % 32 == 0;
+  const bool pipe = !c128 && ra == 256 && allow_pf && use_pipe(t1) && cols % 16 == 0;
+  // (the wide kernel pays only at rho_b >= 128: measured in-place pass at 2^26 .. 2^29, rho_b 32 / 64:
+  //  0.52 / 1.07 / 1.30 / 2.62 ms wide vs 0.30 / 0.58 / 1.16 / 2.32 ms paired; at 2^30, rho_b 128: 4.8-4.9 vs 5.0)
+  const bool wide = !pipe && !c128 && ra == 256 && lb >= 7 && use_wide(t1) && cols % 32 == 0;
   const int F = wide ? 32 : c128 ? 8 : 16, NT = 16 * F;
   const size_t elem = c128 ? 16 : 8;
   if (cols < F || cols % F) return false;
@@ -1161,15 +1697,18 @@ static bool plan_pass(Pass& q, bool t1, int ra, int lb, int64_t cols, int64_t N,
   q.rb = 1 << lb;
   const int64_t R = (int64_t)ra << lb;
   const bool paired = !wide && !c128 && q.ra == 256 && use_pair();
-  q.pf = paired && use_pf(t1) && allow_pf;  // (the sharded entries launch without tensor maps)
+  q.pf = paired && (pipe || use_pf(t1)) && allow_pf;  // (the sharded entries launch without tensor maps)
+  q.pipe = pipe && paired;
   q.fn = reinterpret_cast<void (*)(Args)>(wide ? pick_wide(q.rb, t1)
+                                          : q.pipe ? pick_pipe(q.rb, t1)
                                           : paired ? pick_pair(q.rb, t1, q.pf)
                                           : c128 ? pick<double>(q.ra, q.rb, t1) : pick<float>(q.ra, q.rb, t1));
   if (!q.fn) return false;
-  q.nt = wide ? wide::NT : paired ? pair::NT : NT;
+  q.nt = wide ? wide::NT : q.pipe ? pipe::NT : paired ? pair::NT : NT;
   q.wide = wide;
   // exchange (padded only in the transposing pass) + W_256 + W_R^(i<256) (+ two 192-entry tables)
   q.smem = wide ? (t1 ? wide::SMEM_T1 : wide::SMEM_T0)
+                : q.pipe ? pipe::SMEM
                 : paired ? (int)(((t1 ? pair::XB2 : 4096) + 512) * elem) + (q.pf ? 32768 : 0)
                          : (int)(((t1 ? 256 * (F + 1) : 256 * F) + 512 + (q.ra == 256 ? 0 : 2 * q.ra)) * elem);
   Args& a = q.a;
@@ -1187,6 +1726,7 @@ static bool plan_pass(Pass& q, bool t1, int ra, int lb, int64_t cols, int64_t N,
   const double sc = (!t1 && inverse && scale_inverse) ? 1.0 / (double)N : 1.0;
   a.cout = make_double2(sc, (!t1 && inverse) ? -sc : sc);
   a.check_finite = t1 && check_finite;
+  a.abl = getenv("EFFT_PIPE_ABL") ? atoi(getenv("EFFT_PIPE_ABL")) : 0;
   if (cudaFuncSetAttribute((const void*)q.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, q.smem) != cudaSuccess) {
     *err_cuda = 1;
     return false;
@@ -1208,7 +1748,8 @@ static bool plan_pass(Pass& q, bool t1, int ra, int lb, int64_t cols, int64_t N,
   a.wg = (int32_t)W;
   const int64_t G = a.ngroups / W;
   const int64_t per = ((int64_t)a.ntA + a.ntB) * W;
-  const int64_t window = (4 * (int64_t)q.grid + per - 1) / per;
+  // (pipelined kernel, static schedule: three groups per CTA, two tiles each in flight, the next one probed)
+  const int64_t window = ((q.pipe ? 9 : 4) * (int64_t)q.grid + per - 1) / per;
   int64_t lag = window + 1;
   if (const char* ev = getenv("EFFT_LEAN_LAG")) lag = atoi(ev);
   int64_t slots = wide ? lag + 3 : lag + (window + 1) / 2 + 2;  // super-groups (wide: 8 MB slots, keep <= ~80 MB)

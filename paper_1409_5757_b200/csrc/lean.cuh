@@ -45,6 +45,7 @@ struct Args {
   double2 cin;   // (1, +-1): conjugation of the pass input
   double2 cout;  // (s, +-s): conjugation and scale of the pass output
   int32_t check_finite;
+  int32_t abl;   // dev ablation bits of the pipelined kernel (EFFT_PIPE_ABL; 0 in production)
 };
 
 struct Pass {
@@ -53,7 +54,8 @@ struct Pass {
   int grid, nt, smem;
   int ra, rb;
   bool wide = false;  // 32-column groups (lean_wide)
-  bool pf = false;    // prefetching pair kernel (TMA landing buffer)
+  bool pf = false;    // prefetching pair kernel (TMA landing buffer): needs the tensor maps
+  bool pipe = false;  // pipelined pair kernel (producer warp, two TMA buffers)
   const void* mapA_ptr = nullptr;
   int64_t counter_ints;  // 2 (task counter) + 2 * ngroups
 };
