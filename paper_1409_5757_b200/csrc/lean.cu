@@ -212,10 +212,17 @@ struct Sched {
       sh->task[b] = task;
     }
   }
+  // the next position of this CTA: a dynamic claim, or (a.static_sched) the static
+  // schedule c, c + G, c + 2G, ... -- no claim runs ahead of the tiles in flight
+  long long kpos = 0;
+  __device__ __forceinline__ long long claim(const Args& a) {  // thread 0
+    if (a.static_sched) return blockIdx.x + (kpos++) * (long long)gridDim.x;
+    return (long long)atomicAdd(a.ctr, 1ull);
+  }
   __device__ __forceinline__ void init(const Args& a) {  // all threads
     if (threadIdx.x == 0) {
-      publish(a, 0, (long long)atomicAdd(a.ctr, 1ull));
-      publish(a, 1, (long long)atomicAdd(a.ctr, 1ull));
+      publish(a, 0, claim(a));
+      publish(a, 1, claim(a));
       sh->ready = sh->pos[0] >= a.total || !sh->isB[0] || ld_acquire(a.doneA + sh->g[0]) >= a.ntA;
     }
     __syncthreads();
@@ -237,7 +244,7 @@ struct Sched {
       __syncthreads();
     }
     if (threadIdx.x == 0) {
-      claim2 = (long long)atomicAdd(a.ctr, 1ull);
+      claim2 = claim(a);
       const int nb = cb ^ 1;
       nxt_val = 0;
       slot_val = a.ntB;
@@ -1727,6 +1734,7 @@ static bool plan_pass(Pass& q, bool t1, int ra, int lb, int64_t cols, int64_t N,
   a.cout = make_double2(sc, (!t1 && inverse) ? -sc : sc);
   a.check_finite = t1 && check_finite;
   a.abl = getenv("EFFT_PIPE_ABL") ? atoi(getenv("EFFT_PIPE_ABL")) : 0;
+  a.static_sched = getenv("EFFT_LEAN_STATIC") ? atoi(getenv("EFFT_LEAN_STATIC")) : 0;
   if (cudaFuncSetAttribute((const void*)q.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, q.smem) != cudaSuccess) {
     *err_cuda = 1;
     return false;
