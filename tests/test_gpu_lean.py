@@ -182,3 +182,51 @@ def test_lean_minimal_ring_is_deadlock_free_and_exact(n, dtype, lag, slots, monk
     p, y = run(x, dtype)
     assert f"lag={lag} slots={slots}" in p.describe()
     assert torch.equal(y, ref)  # deterministic: same arithmetic, any schedule
+
+
+@pytest.mark.parametrize("lg", [24, 26, 27])
+def test_pipelined_kernel_vs_oracle_and_default_path(lg, monkeypatch):
+    """EFFT_LEAN_PIPE=3: the TMA-fed pipelined pair kernel (one CTA per SM, three
+    compute groups, issue warps + a release lane, static schedule) in both passes:
+    same arithmetic as the default kernels, so bit-identical output, both directions."""
+    n = 1 << lg
+    x = random_c(n, seed=lg + 7)
+    xd = torch.from_numpy(x.astype(np.complex64)).cuda()
+    _, ref = run(xd, "complex64")
+    _, iref = run(ref, "complex64", direction=1)
+    monkeypatch.setenv("EFFT_LEAN_PIPE", "3")
+    p, y = run(xd, "complex64", flags=_native.EFFT_FLAG_CHECK_FINITE)
+    assert "x 512" in p.describe()  # 3 x 128 compute threads + 4 service warps
+    assert not p.nonfinite_seen(torch.cuda.current_stream().cuda_stream)
+    assert oracle.rel_l2(y.cpu().numpy(), oracle.transform(x)) <= tol(n, "complex64")
+    assert torch.equal(y, ref)
+    _, z = run(y, "complex64", direction=1)
+    assert torch.equal(z, iref)
+    assert oracle.rel_l2(z.cpu().numpy(), x) <= 2 * tol(n, "complex64")
+
+
+@pytest.mark.parametrize("lag,slots", [(1, 2), (2, 3), (4, 6)])
+def test_pipelined_kernel_minimal_ring_and_repeats(lag, slots, monkeypatch):
+    """The pipelined kernel under maximal dependency pressure, run repeatedly (its
+    mbarrier rings must never be overrun whatever the timing), and its non-finite flag."""
+    n = 1 << 25
+    x = torch.from_numpy(random_c(n, seed=5).astype(np.complex64)).cuda()
+    _, ref = run(x, "complex64")
+    monkeypatch.setenv("EFFT_LEAN_PIPE", "3")
+    monkeypatch.setenv("EFFT_LEAN_LAG", str(lag))
+    monkeypatch.setenv("EFFT_LEAN_SLOTS", str(slots))
+    p = _native.NativePlan(n, _native.EFFT_C64, -1, 0, _native.EFFT_FLAG_CHECK_FINITE)
+    assert f"lag={lag} slots={slots}" in p.describe()
+    s = torch.cuda.current_stream().cuda_stream
+    y = torch.empty_like(x)
+    for _ in range(8):
+        y.zero_()
+        p.execute(x.data_ptr(), y.data_ptr(), s)
+    torch.cuda.synchronize()
+    assert torch.equal(y, ref)
+    assert not p.nonfinite_seen(s)
+    xb = x.clone()
+    xb[12345] = complex(float("inf"), 0.0)
+    p.execute(xb.data_ptr(), y.data_ptr(), s)
+    torch.cuda.synchronize()
+    assert p.nonfinite_seen(s)
