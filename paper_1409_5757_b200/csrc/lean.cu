@@ -256,8 +256,17 @@ struct Sched {
   // thread 0, right after issuing the tile loads: one fence (acquire of the
   // probes, release of the previous tile).  Warp 0 waits for its loads here
   // anyway, so the fence costs no extra time on the critical path.
-  __device__ __forceinline__ void after_loads(const Args&, int, int) {
-    if (threadIdx.x == 0) sy.fence_release();
+  __device__ __forceinline__ void after_loads(const Args& a, int, int) {
+    if (threadIdx.x == 0) {
+      if (a.abl & 2048) {  // dev ablation (timing only): no fence
+        if (sy.pend != nullptr) {
+          asm volatile("red.relaxed.gpu.global.add.s32 [%0], 1;" ::"l"(sy.pend) : "memory");
+          sy.pend = nullptr;
+        }
+      } else {
+        sy.fence_release();
+      }
+    }
   }
   // thread 0, before the exchange barrier: this A tile may store once its
   // staging slot is free (rarely not yet)
@@ -524,6 +533,9 @@ __global__ void __launch_bounds__(pair::NT, PF ? 3 : 4) lean_pair(const __grid_c
   float4* xq = reinterpret_cast<float4*>(xbase);
   V* w256 = xb + (T1 ? pair::XB2 : 4096);  // the plain exchange needs no padding
   V* wlo = w256 + 256;
+  // T1 B tiles: the tile's four-step twiddle factors, built once per tile in fp64 (below)
+  __shared__ double2 twc[T1 ? DB * 8 : 1], twq[T1 ? 16 : 1], tws[T1 ? DB : 1];
+  __shared__ float2 twj[T1 ? DB : 1];
   __shared__ SchedShared shs;
   __shared__ __align__(8) uint64_t lbar;
   __shared__ int pf_sh[2];
@@ -670,6 +682,33 @@ __global__ void __launch_bounds__(pair::NT, PF ? 3 : 4) lean_pair(const __grid_c
           }
         }
       }
+      if constexpr (T1) {
+        // W_N^(j2 k1), k1 = c + 256 QB kp, c = (2cp + 16 ks) + 256 kq, from exact integer
+        // exponents in fp64 (north star c), factored so that a tile needs 10 DB + 16
+        // sincospi instead of three per thread:
+        //   twc[dl][cp] = W_N^(j2 (2cp + 16 ks)),  twq[dl][kq] = W_N^(j2 256 kq),
+        //   tws[dl] = W_N^(j2 256 QB) (the recurrence step),  twj[dl] = W_N^(j2) (column kt + 1)
+        const uint64_t N = (uint64_t)a.N;
+        const int ks = task & 15;
+        for (int i = tid; i < DB * 8 + 16 + 2 * DB; i += pair::NT) {
+          int dl2, kind, idx;
+          if (i < DB * 8) {
+            kind = 0, dl2 = i >> 3, idx = i & 7;
+          } else if (i < DB * 8 + 16) {
+            kind = 1, dl2 = (i - DB * 8) / QB, idx = (i - DB * 8) % QB;
+          } else {
+            kind = 2 + ((i - DB * 8 - 16) >= DB), dl2 = (i - DB * 8 - 16) % DB, idx = 0;
+          }
+          const uint64_t jg = (uint64_t)(a.j2off + g * 16 + (task >> 4) * DB + dl2);  // global column
+          const uint64_t m = kind == 0 ? (uint64_t)(2 * idx + 16 * ks) : kind == 1 ? (uint64_t)(256 * idx)
+                             : kind == 2 ? (uint64_t)(256 * QB) : 1ull;
+          const double2 w = wroot((int64_t)((jg * m) % N), a.N);
+          if (kind == 0) twc[i] = w;
+          else if (kind == 1) twq[i - DB * 8] = w;
+          else if (kind == 2) tws[dl2] = w;
+          else twj[dl2] = to_v(w, 0.f);
+        }
+      }
       // consumed staging lines: 8 threads share a line, thread cp drops the
       // lines of its loads cp and cp + 8
 #pragma unroll
@@ -684,9 +723,15 @@ __global__ void __launch_bounds__(pair::NT, PF ? 3 : 4) lean_pair(const __grid_c
     } else {
       // ---- A stage 0: 16-point DFTs over t, W_256^(s kt) shared by the pair
       if (a.check_finite) {
+        // v * 0 is +-0 for a finite v and NaN for +-Inf / NaN: one FFMA2 per complex value
+        V acc = make_float2(0.f, 0.f);
+        const V zero = make_float2(0.f, 0.f);
 #pragma unroll
-        for (int t = 0; t < 16; ++t)
-          nf |= !(isfinite(x[t].x) && isfinite(x[t].y) && isfinite(y[t].x) && isfinite(y[t].y));
+        for (int t = 0; t < 16; ++t) {
+          acc = fma2(x[t], zero, acc);
+          acc = fma2(y[t], zero, acc);
+        }
+        nf |= !(acc.x == 0.f && acc.y == 0.f);
       }
       if constexpr (T1) {
         if (a.cin.y != 1.0) {  // inverse: conjugate the input (forward: identity)
@@ -743,10 +788,9 @@ __global__ void __launch_bounds__(pair::NT, PF ? 3 : 4) lean_pair(const __grid_c
         // fp64 bases and step (sincospi), fp64 recurrence, one rounding per
         // use -- fp64-accurate twiddles on the fp32 path, no table (north star c)
         // (column kt + 1: times W_N^j2 in fp32, <= 1.5 ulp)
-        const uint64_t N = (uint64_t)a.N, jg = (uint64_t)(a.j2off + j2);  // global column
-        double2 w0 = wroot((int64_t)((jg * c) % N), a.N);
-        const V wj = to_v(wroot((int64_t)(jg % N), a.N), 0.f);
-        const double2 st = wroot((int64_t)((jg * (256 * QB)) % N), a.N);
+        double2 w0 = cmul(twc[dl * 8 + cp], twq[dl * QB + kq]);
+        const V wj = twj[dl];
+        const double2 st = tws[dl];
         if (a.obl == 0) {  // y[k1 + R j2]: one base pointer, immediate offsets
           V* op = DST + (int64_t)j2 * a.R + c;
 #pragma unroll
@@ -1134,9 +1178,15 @@ __global__ void __launch_bounds__(pipe::NT, 1) lean_pipe(const __grid_constant__
     } else {
       // ---- A stage 0: 16-point DFTs over t, W_256^(s kt) shared by the pair
       if (a.check_finite) {
+        // v * 0 is +-0 for a finite v and NaN for +-Inf / NaN: one FFMA2 per complex value
+        V acc = make_float2(0.f, 0.f);
+        const V zero = make_float2(0.f, 0.f);
 #pragma unroll
-        for (int t = 0; t < 16; ++t)
-          nf |= !(isfinite(x[t].x) && isfinite(x[t].y) && isfinite(y[t].x) && isfinite(y[t].y));
+        for (int t = 0; t < 16; ++t) {
+          acc = fma2(x[t], zero, acc);
+          acc = fma2(y[t], zero, acc);
+        }
+        nf |= !(acc.x == 0.f && acc.y == 0.f);
       }
       if constexpr (T1) {
         if (a.cin.y != 1.0) {  // inverse: conjugate the input (forward: identity)
@@ -1467,9 +1517,15 @@ __global__ void __launch_bounds__(wide::NT, 2) lean_wide(const __grid_constant__
     } else {
       // ---- A stage 0: 16-point DFTs over t, W_256^(s kt) shared by the pair
       if (a.check_finite) {
+        // v * 0 is +-0 for a finite v and NaN for +-Inf / NaN: one FFMA2 per complex value
+        V acc = make_float2(0.f, 0.f);
+        const V zero = make_float2(0.f, 0.f);
 #pragma unroll
-        for (int t = 0; t < 16; ++t)
-          nf |= !(isfinite(x[t].x) && isfinite(x[t].y) && isfinite(y[t].x) && isfinite(y[t].y));
+        for (int t = 0; t < 16; ++t) {
+          acc = fma2(x[t], zero, acc);
+          acc = fma2(y[t], zero, acc);
+        }
+        nf |= !(acc.x == 0.f && acc.y == 0.f);
       }
       if constexpr (T1) {
         if (a.cin.y != 1.0) {  // inverse: conjugate the input (forward: identity)
