@@ -165,8 +165,15 @@ struct efft_plan_s {
     int32_t* flag = nullptr;
     void* work = nullptr;  // N / G elements
     cudaEvent_t ev = nullptr;
+    // overlapped execution (sh_chunks > 1): a second work array (exchange 2 lands
+    // while pass 1 still reads `work`), a copy stream, and per-chunk events
+    // [exchange 1 in, pass 1, exchange 2 out, pass 2, exchange 3 out]
+    void* work2 = nullptr;
+    cudaStream_t cs = nullptr, cs2 = nullptr;  // incoming (exchange 1) / outgoing (exchanges 2, 3) copies
+    std::vector<cudaEvent_t> cev;
   };
   std::vector<Rank> ranks;
+  int sh_chunks = 1;
   int64_t sh_n1 = 0, sh_n2 = 0;
   int sh_rank = 0, sh_world = 0;  // shard-rank plans (efft_plan_create_shard_rank)
 };
@@ -1232,10 +1239,11 @@ int efft_plan_launch_times(efft_plan_t pl, float* ms, int max_launches) {
   return EFFT_OK;
 }
 
-static int launch_lean(efft::lean::Pass& q, const void* src, void* dst, cudaStream_t s) {
+static int launch_lean(efft::lean::Pass& q, const void* src, void* dst, cudaStream_t s, int64_t j2shift = 0) {
   efft::lean::Args a = q.a;
   a.src = src;
   a.dst = dst;
+  a.j2off += j2shift;  // column chunk of the transposing pass: global column of its first column
   q.fn<<<q.grid, q.nt, q.smem, s>>>(a);
   CUDA_TRY(cudaGetLastError());
   return EFFT_OK;
@@ -1271,6 +1279,16 @@ int efft_plan_create_sharded(efft_plan_t* out, int64_t n, int dtype, int directi
   pl->sh_n2 = N2;
   pl->ranks.resize(ngpus);
   const size_t local = (size_t)(n / ngpus) * pl->elem;
+  // Column chunks of the overlapped schedule (EFFT_SHARD_CHUNKS, default 4): every
+  // chunk keeps whole lane groups and at least 16 of them; 1 = the sequential schedule
+  int chunks = env_int("EFFT_SHARD_CHUNKS", 4);
+  {
+    const int64_t L1 = N1 / ngpus, L2 = N2 / ngpus, F = efft::lean::lanes(c128);
+    if (chunks < 1) chunks = 1;
+    while (chunks > 1 && (L1 % (chunks * F) || L2 % (chunks * F) || L1 / (chunks * F) < 16 || L2 / (chunks * F) < 16))
+      chunks /= 2;
+  }
+  pl->sh_chunks = chunks;
   for (int q = 0; q < ngpus; ++q) {
     auto& r = pl->ranks[q];
     r.dev = devices[q];
@@ -1282,7 +1300,7 @@ int efft_plan_create_sharded(efft_plan_t* out, int64_t n, int dtype, int directi
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, r.dev);
     int64_t stg = 0;
     if (!efft::lean::plan_sharded(n, ngpus, q, c128, direction == EFFT_INVERSE, (flags & EFFT_FLAG_CHECK_FINITE) != 0,
-                                  sms, r.lp, &stg, &ecuda)) {
+                                  sms, r.lp, &stg, &ecuda, false, chunks)) {
       efft_plan_destroy(pl);
       return ecuda ? fail(EFFT_ERR_CUDA, "sharded pass setup failed") : fail(EFFT_ERR_UNSUPPORTED_SIZE, "no pass kernel");
     }
@@ -1294,6 +1312,18 @@ int efft_plan_create_sharded(efft_plan_t* out, int64_t n, int dtype, int directi
       cudaGetLastError();
       efft_plan_destroy(pl);
       return fail(EFFT_ERR_ALLOC, "sharded rank %d buffers (%zu bytes + ring)", q, local);
+    }
+    if (chunks > 1) {
+      bool ok = cudaMalloc(&r.work2, local) == cudaSuccess &&
+                cudaStreamCreateWithFlags(&r.cs, cudaStreamNonBlocking) == cudaSuccess &&
+                cudaStreamCreateWithFlags(&r.cs2, cudaStreamNonBlocking) == cudaSuccess;
+      r.cev.assign((size_t)5 * chunks, nullptr);
+      for (auto& e : r.cev) ok = ok && cudaEventCreateWithFlags(&e, cudaEventDisableTiming) == cudaSuccess;
+      if (!ok) {
+        cudaGetLastError();
+        efft_plan_destroy(pl);
+        return fail(EFFT_ERR_ALLOC, "sharded rank %d overlap buffers (%zu bytes)", q, local);
+      }
     }
     int64_t off = 0;
     for (auto& ps : r.lp) {
@@ -1349,6 +1379,78 @@ int efft_execute_sharded(efft_plan_t pl, const void* const* in, void* const* out
   };
   int rc = all_wait();
   if (rc != EFFT_OK) return rc;
+  if (pl->sh_chunks > 1) {
+    // Overlapped schedule: the local passes run in C column chunks on the caller's
+    // streams while the exchanges of the neighbouring chunks run on per-rank copy
+    // streams (pitched peer copies over NVLink):
+    //   exchange 1 chunk i+1  ||  pass 1 chunk i  ||  exchange 2 slab i-1
+    //   pass 2 chunk j        ||  exchange 3 slab j-1
+    // Exchange 2 lands in a second work array (pass 1 of the destination may still be
+    // reading its first one).  Exposed: the first chunk of exchange 1, the last slab of
+    // exchange 2 (pass 2 needs every row) and the last slab of exchange 3.
+    const int C = pl->sh_chunks;
+    const int64_t c2 = L2 / C, c1 = L1 / C;
+    auto CS = [&](int q) { return pl->ranks[q].cs; };
+    auto CO = [&](int q) { return pl->ranks[q].cs2; };
+    auto W2 = [&](int q) { return (char*)pl->ranks[q].work2; };
+    auto EV = [&](int q, int kind, int i) { return pl->ranks[q].cev[(size_t)kind * C + i]; };
+    for (int q = 0; q < G; ++q) {
+      auto& rk = pl->ranks[q];
+      CUDA_TRY(cudaSetDevice(rk.dev));
+      // the copy stream starts where the rank's stream is (behind every rank's previous work)
+      CUDA_TRY(cudaEventRecord(rk.ev, S(q)));
+      CUDA_TRY(cudaStreamWaitEvent(CS(q), rk.ev, 0));
+      CUDA_TRY(cudaStreamWaitEvent(CO(q), rk.ev, 0));
+      for (int i = 0; i < C; ++i) {  // exchange 1, column chunk i: B_q[p L1 + r][i c2 + c] = x_p[r][q L2 + i c2 + c]
+        for (int p = 0; p < G; ++p)
+          CUDA_TRY(cudaMemcpy2DAsync(W(q) + (size_t)(p * L1 * L2 + i * c2) * e, L2 * e,
+                                     (const char*)in[p] + (size_t)(q * L2 + i * c2) * e, N2 * e, c2 * e, L1,
+                                     cudaMemcpyDefault, CS(q)));
+        CUDA_TRY(cudaEventRecord(EV(q, 0, i), CS(q)));
+      }
+      for (int i = 0; i < C; ++i) {  // pass 1, chunk i: columns [i c2, (i+1) c2) -> rows of Y'_q (in out_q)
+        CUDA_TRY(cudaStreamWaitEvent(S(q), EV(q, 0, i), 0));
+        CUDA_TRY(cudaMemsetAsync(rk.lp[0].a.ctr, 0, (size_t)rk.lp[0].counter_ints * 4, S(q)));
+        rc = launch_lean(rk.lp[0], W(q) + (size_t)(i * c2) * e, (char*)out[q] + (size_t)(i * c2 * N1) * e, S(q), i * c2);
+        if (rc != EFFT_OK) return rc;
+        CUDA_TRY(cudaEventRecord(EV(q, 1, i), S(q)));
+      }
+      for (int i = 0; i < C; ++i) {  // exchange 2, slab i (pushed): T_p[q L2 + i c2 + c][k1'] = Y'_q[i c2 + c][p L1 + k1']
+        CUDA_TRY(cudaStreamWaitEvent(CO(q), EV(q, 1, i), 0));
+        for (int p = 0; p < G; ++p)
+          CUDA_TRY(cudaMemcpy2DAsync(W2(p) + (size_t)((q * L2 + i * c2) * L1) * e, L1 * e,
+                                     (const char*)out[q] + (size_t)(i * c2 * N1 + p * L1) * e, N1 * e, L1 * e, c2,
+                                     cudaMemcpyDefault, CO(q)));
+        CUDA_TRY(cudaEventRecord(EV(q, 2, i), CO(q)));
+      }
+    }
+    for (int p = 0; p < G; ++p) {
+      auto& rk = pl->ranks[p];
+      CUDA_TRY(cudaSetDevice(rk.dev));
+      for (int q = 0; q < G; ++q)
+        for (int i = 0; i < C; ++i) CUDA_TRY(cudaStreamWaitEvent(S(p), EV(q, 2, i), 0));
+      for (int j = 0; j < C; ++j) {  // pass 2 in place on T_p, column chunk j
+        CUDA_TRY(cudaMemsetAsync(rk.lp[1].a.ctr, 0, (size_t)rk.lp[1].counter_ints * 4, S(p)));
+        rc = launch_lean(rk.lp[1], W2(p) + (size_t)(j * c1) * e, W2(p) + (size_t)(j * c1) * e, S(p));
+        if (rc != EFFT_OK) return rc;
+        CUDA_TRY(cudaEventRecord(EV(p, 3, j), S(p)));
+        // exchange 3, slab j (pushed): y_r[k2'][p L1 + j c1 + k1'] = X_p[r L2 + k2'][j c1 + k1'].  out_r is free:
+        // pass 2 anywhere implies every rank's exchange 2 has left it
+        CUDA_TRY(cudaStreamWaitEvent(CO(p), EV(p, 3, j), 0));
+        for (int r = 0; r < G; ++r)
+          CUDA_TRY(cudaMemcpy2DAsync((char*)out[r] + (size_t)(p * L1 + j * c1) * e, N1 * e,
+                                     W2(p) + (size_t)(r * L2 * L1 + j * c1) * e, L1 * e, c1 * e, L2, cudaMemcpyDefault,
+                                     CO(p)));
+        CUDA_TRY(cudaEventRecord(EV(p, 4, j), CO(p)));
+      }
+    }
+    for (int r = 0; r < G; ++r) {  // every rank's stream ends behind every exchange-3 slab
+      CUDA_TRY(cudaSetDevice(pl->ranks[r].dev));
+      for (int p = 0; p < G; ++p)
+        for (int j = 0; j < C; ++j) CUDA_TRY(cudaStreamWaitEvent(S(r), EV(p, 4, j), 0));
+    }
+    return all_wait();
+  }
   // exchange 1 (pulled by the destination): B_q[p L1 + r][c] = x_p[r][q L2 + c]
   for (int q = 0; q < G; ++q) {
     CUDA_TRY(cudaSetDevice(pl->ranks[q].dev));
@@ -1474,6 +1576,11 @@ int efft_plan_destroy(efft_plan_t pl) {
     if (r.counters) cudaFree(r.counters);
     if (r.flag) cudaFree(r.flag);
     if (r.work) cudaFree(r.work);
+    if (r.work2) cudaFree(r.work2);
+    if (r.cs) cudaStreamDestroy(r.cs);
+    if (r.cs2) cudaStreamDestroy(r.cs2);
+    for (auto& e : r.cev)
+      if (e) cudaEventDestroy(e);
     if (r.ev) cudaEventDestroy(r.ev);
   }
   cudaSetDevice(pl->device);

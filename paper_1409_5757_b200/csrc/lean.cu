@@ -1864,6 +1864,8 @@ bool plan(int64_t n, int c128, int inverse, bool scale_inverse, bool check_finit
   return true;
 }
 
+int lanes(int c128) { return c128 ? 8 : 32; }
+
 bool split_sharded(int64_t n, int G, int c128, int64_t* N1, int64_t* N2) {
   int m, t;
   if (!factor_m(n, m, t) || G < 1 || (G & (G - 1))) return false;
@@ -1878,7 +1880,7 @@ bool split_sharded(int64_t n, int G, int c128, int64_t* N1, int64_t* N2) {
 }
 
 bool plan_sharded(int64_t n, int G, int rank, int c128, int inverse, bool check_finite, int num_sms, Pass p[2],
-                  int64_t* staging_elems, int* err_cuda, bool blocked) {
+                  int64_t* staging_elems, int* err_cuda, bool blocked, int chunks) {
   *err_cuda = 0;
   int64_t N1, N2;
   if (!split_sharded(n, G, c128, &N1, &N2)) return false;
@@ -1889,11 +1891,17 @@ bool plan_sharded(int64_t n, int G, int rank, int c128, int inverse, bool check_
   while ((int64_t(256) << lb1) < N1) ++lb1;
   while (((int64_t)ra2 << lb2) < N2) ++lb2;
   const int64_t L1 = N1 / G, L2 = N2 / G;
-  // pass 1 over this rank's L2 columns (global columns rank * L2 + c), pass 2 over its L1 columns
-  if (!plan_pass(p[0], true, 256, lb1, L2, n, (int64_t)rank * L2, c128, inverse, true, check_finite, num_sms,
-                 err_cuda, false) ||
-      !plan_pass(p[1], false, ra2, lb2, L1, n, 0, c128, inverse, true, check_finite, num_sms, err_cuda, false))
+  // pass 1 over this rank's L2 columns (global columns rank * L2 + c), pass 2 over its L1 columns;
+  // chunks > 1 (the overlapped single-process entry): each launch covers 1 / chunks of the
+  // columns -- the row strides stay L2 and L1, the launcher offsets src / dst / j2off
+  if (chunks < 1 || L2 % chunks || L1 % chunks) return false;
+  if (!plan_pass(p[0], true, 256, lb1, L2 / chunks, n, (int64_t)rank * L2, c128, inverse, true, check_finite,
+                 num_sms, err_cuda, false) ||
+      !plan_pass(p[1], false, ra2, lb2, L1 / chunks, n, 0, c128, inverse, true, check_finite, num_sms, err_cuda,
+                 false))
     return false;
+  p[0].a.LS = L2;
+  p[1].a.LS = L1;
   if (blocked) {
     int lg = 0;
     while ((int64_t(1) << lg) < L1) ++lg;

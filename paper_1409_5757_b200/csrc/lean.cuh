@@ -76,7 +76,9 @@ bool split_sharded(int64_t n, int G, int c128, int64_t* N1, int64_t* N2);
 int encode_input(Pass& p, const void* src);
 int encode_ring(Pass& p, void* staging);
 bool plan_sharded(int64_t n, int G, int rank, int c128, int inverse, bool check_finite, int num_sms, Pass p[2],
-                  int64_t* staging_elems, int* err_cuda, bool blocked = false);
+                  int64_t* staging_elems, int* err_cuda, bool blocked = false, int chunks = 1);
+// columns per lane group (one 128-byte line; 32 for the wide complex64 kernel): chunk widths must be multiples
+int lanes(int c128);
 
 }  // namespace lean
 }  // namespace efft
