@@ -311,6 +311,8 @@ __global__ void __launch_bounds__(LT<R>::NT, MINB) lean_pass(const __grid_consta
   V* whi = RA == 256 ? w256 : wlo + 256;
   V* wa = RA == 256 ? w256 : wlo + 256 + RA;
   constexpr int HS = RA == 256 ? 256 / RB : 1;  // stride of whi
+  // T1 B tiles: the tile's four-step twiddle factors, built once per tile in fp64 (below)
+  __shared__ double2 twc[T1 ? DB * F : 1], twq[T1 ? 16 : 1], tws[T1 ? DB : 1];
   __shared__ SchedShared shs;
   const int tid = threadIdx.x, lane = tid % F, r = tid / F;
   // kernel parameters stay in the constant bank (read at use, no registers held)
@@ -380,6 +382,32 @@ __global__ void __launch_bounds__(LT<R>::NT, MINB) lean_pass(const __grid_consta
           for (int dl = 0; dl < DB; ++dl) v[dl * QB + P<QB>(k)] = cmul(v[dl * QB + P<QB>(k)], w);
         }
       }
+      if constexpr (T1) {
+        // W_N^(j2 k1), k1 = c + RA QB kp, c = (h F + lane + 16 ks) + RA kq, from exact integer
+        // exponents in fp64, factored so that a tile needs DB (F + QB + 1) sincospi instead of
+        // two per thread: twc[dl][lane] = W_N^(j2 (h F + lane + 16 ks)), twq[dl][kq] = W_N^(j2 RA kq),
+        // tws[dl] = W_N^(j2 RA QB) (the recurrence step)
+        int ks, h, jblk;
+        t1_task<F, S>(task, ks, h, jblk);
+        const uint64_t N = (uint64_t)a.N;
+        for (int i = tid; i < DB * F + 16 + DB; i += NT) {
+          int dl2, kind, idx;
+          if (i < DB * F) {
+            kind = 0, dl2 = i / F, idx = i % F;
+          } else if (i < DB * F + 16) {
+            kind = 1, dl2 = (i - DB * F) / QB, idx = (i - DB * F) % QB;
+          } else {
+            kind = 2, dl2 = i - DB * F - 16, idx = 0;
+          }
+          const uint64_t jg = (uint64_t)(a.j2off + g * F + jblk * DB + dl2);  // global column
+          const uint64_t m = kind == 0 ? (uint64_t)(h * F + idx + 16 * ks) : kind == 1 ? (uint64_t)(RA * idx)
+                                                                                       : (uint64_t)(RA * QB);
+          const double2 w = wroot((int64_t)((jg * m) % N), a.N);
+          if (kind == 0) twc[i] = w;
+          else if (kind == 1) twq[i - DB * F] = w;
+          else tws[dl2] = w;
+        }
+      }
       // the consumed staging lines leave L2 without write-back: F lanes share
       // a line, lane i drops the lines of its loads i, i + F, ...
 #pragma unroll
@@ -434,9 +462,8 @@ __global__ void __launch_bounds__(LT<R>::NT, MINB) lean_pass(const __grid_consta
         const uint32_t c = (uint32_t)(h * F + lane + 16 * ks + RA * kq);
         // W_N^(j2 k1) from the exact integer exponent: fp64 base and step
         // (sincospi), fp64 recurrence, one rounding per use (north star c)
-        const uint64_t jg = (uint64_t)(a.j2off + j2);  // global column (sharded: rank offset)
-        double2 w = wroot((int64_t)((jg * c) % (uint64_t)a.N), a.N);
-        const double2 st = wroot((int64_t)((jg * (RA * QB)) % (uint64_t)a.N), a.N);
+        double2 w = cmul(twc[dl * F + lane], twq[dl * QB + kq]);
+        const double2 st = tws[dl];
         V* op = DST + (int64_t)j2 * a.R + c;
 #pragma unroll
         for (int kp = 0; kp < 16; ++kp) {

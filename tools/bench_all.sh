@@ -19,6 +19,6 @@ python bench.py --steps 2 --warmup 3 --no-cpu --no-e2e --no-parity > $out/plain.
 ncu --metrics gpu__time_duration.sum --clock-control none -c 60 --csv --log-file $out/c3_launches.csv \
   python bench.py --steps 2 --warmup 3 --no-cpu --no-e2e --no-parity > $out/ncu_launch.log 2>&1
 echo "ncu launches rc=$?"
-ncu --set full --clock-control none --import-source on -k regex:lean_pair -s 2 -c 2 -o $out/c3_full \
+ncu --set full --clock-control none --import-source on -k regex:lean_ -s 2 -c 2 -o $out/c3_full \
   python bench.py --steps 2 --warmup 3 --no-cpu --no-e2e --no-parity > $out/ncu_full.log 2>&1
 echo "ncu full rc=$?"
