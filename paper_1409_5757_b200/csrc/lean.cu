@@ -1841,9 +1841,11 @@ static bool plan_pass(Pass& q, bool t1, int ra, int lb, int64_t cols, int64_t N,
   const int64_t per = ((int64_t)a.ntA + a.ntB) * W;
   // (pipelined kernel, static schedule: three groups per CTA, two tiles each in flight, the next one probed)
   const int64_t window = ((q.pipe ? 9 : 4) * (int64_t)q.grid + per - 1) / per;
-  int64_t lag = window + 1;
+  // (measured at 2^30: paired 10:16 4.97 / 4.77 ms vs 11:18 5.06 / 4.89 and 13:20 5.44 / 5.13;
+  //  wide in-place pass 5:8 4.62 ms vs 6:9 4.69 and 8:12 5.16 -- the ring must stay well inside L2)
+  int64_t lag = window + (getenv("EFFT_LEAN_LAGPLUS") ? atoi(getenv("EFFT_LEAN_LAGPLUS")) : 0);
   if (const char* ev = getenv("EFFT_LEAN_LAG")) lag = atoi(ev);
-  int64_t slots = wide ? lag + 3 : lag + (window + 1) / 2 + 2;  // super-groups (wide: 8 MB slots, keep <= ~80 MB)
+  int64_t slots = wide ? lag + 3 : lag + (window + 1) / 2 + 1;  // super-groups (wide: 8 MB slots)
   if (const char* ev = getenv("EFFT_LEAN_SLOTS")) slots = atoi(ev);
   if (lag < 1) lag = 1;
   if (lag > G) lag = G;
