@@ -212,17 +212,10 @@ struct Sched {
       sh->task[b] = task;
     }
   }
-  // the next position of this CTA: a dynamic claim, or (a.static_sched) the static
-  // schedule c, c + G, c + 2G, ... -- no claim runs ahead of the tiles in flight
-  long long kpos = 0;
-  __device__ __forceinline__ long long claim(const Args& a) {  // thread 0
-    if (a.static_sched) return blockIdx.x + (kpos++) * (long long)gridDim.x;
-    return (long long)atomicAdd(a.ctr, 1ull);
-  }
   __device__ __forceinline__ void init(const Args& a) {  // all threads
     if (threadIdx.x == 0) {
-      publish(a, 0, claim(a));
-      publish(a, 1, claim(a));
+      publish(a, 0, (long long)atomicAdd(a.ctr, 1ull));
+      publish(a, 1, (long long)atomicAdd(a.ctr, 1ull));
       sh->ready = sh->pos[0] >= a.total || !sh->isB[0] || ld_acquire(a.doneA + sh->g[0]) >= a.ntA;
     }
     __syncthreads();
@@ -244,7 +237,7 @@ struct Sched {
       __syncthreads();
     }
     if (threadIdx.x == 0) {
-      claim2 = claim(a);
+      claim2 = (long long)atomicAdd(a.ctr, 1ull);
       const int nb = cb ^ 1;
       nxt_val = 0;
       slot_val = a.ntB;
@@ -256,17 +249,8 @@ struct Sched {
   // thread 0, right after issuing the tile loads: one fence (acquire of the
   // probes, release of the previous tile).  Warp 0 waits for its loads here
   // anyway, so the fence costs no extra time on the critical path.
-  __device__ __forceinline__ void after_loads(const Args& a, int, int) {
-    if (threadIdx.x == 0) {
-      if (a.abl & 2048) {  // dev ablation (timing only): no fence
-        if (sy.pend != nullptr) {
-          asm volatile("red.relaxed.gpu.global.add.s32 [%0], 1;" ::"l"(sy.pend) : "memory");
-          sy.pend = nullptr;
-        }
-      } else {
-        sy.fence_release();
-      }
-    }
+  __device__ __forceinline__ void after_loads(const Args&, int, int) {
+    if (threadIdx.x == 0) sy.fence_release();
   }
   // thread 0, before the exchange barrier: this A tile may store once its
   // staging slot is free (rarely not yet)
@@ -312,7 +296,10 @@ __global__ void __launch_bounds__(LT<R>::NT, MINB) lean_pass(const __grid_consta
   V* wa = RA == 256 ? w256 : wlo + 256 + RA;
   constexpr int HS = RA == 256 ? 256 / RB : 1;  // stride of whi
   // T1 B tiles: the tile's four-step twiddle factors, built once per tile in fp64 (below)
-  __shared__ double2 twc[T1 ? DB * F : 1], twq[T1 ? 16 : 1], tws[T1 ? DB : 1];
+  // (complex128 only: the complex64 instantiation of this kernel is a fallback behind lean_pair
+  // and would spill with the extra addressing)
+  constexpr bool TWT = T1 && sizeof(R) == 8;
+  __shared__ double2 twc[TWT ? DB * F : 1], twq[TWT ? 16 : 1], tws[TWT ? DB : 1];
   __shared__ SchedShared shs;
   const int tid = threadIdx.x, lane = tid % F, r = tid / F;
   // kernel parameters stay in the constant bank (read at use, no registers held)
@@ -382,7 +369,7 @@ __global__ void __launch_bounds__(LT<R>::NT, MINB) lean_pass(const __grid_consta
           for (int dl = 0; dl < DB; ++dl) v[dl * QB + P<QB>(k)] = cmul(v[dl * QB + P<QB>(k)], w);
         }
       }
-      if constexpr (T1) {
+      if constexpr (TWT) {
         // W_N^(j2 k1), k1 = c + RA QB kp, c = (h F + lane + 16 ks) + RA kq, from exact integer
         // exponents in fp64, factored so that a tile needs DB (F + QB + 1) sincospi instead of
         // two per thread: twc[dl][lane] = W_N^(j2 (h F + lane + 16 ks)), twq[dl][kq] = W_N^(j2 RA kq),
@@ -462,8 +449,15 @@ __global__ void __launch_bounds__(LT<R>::NT, MINB) lean_pass(const __grid_consta
         const uint32_t c = (uint32_t)(h * F + lane + 16 * ks + RA * kq);
         // W_N^(j2 k1) from the exact integer exponent: fp64 base and step
         // (sincospi), fp64 recurrence, one rounding per use (north star c)
-        double2 w = cmul(twc[dl * F + lane], twq[dl * QB + kq]);
-        const double2 st = tws[dl];
+        double2 w, st;
+        if constexpr (TWT) {
+          w = cmul(twc[dl * F + lane], twq[dl * QB + kq]);
+          st = tws[dl];
+        } else {
+          const uint64_t jg = (uint64_t)(a.j2off + j2);  // global column (sharded: rank offset)
+          w = wroot((int64_t)((jg * c) % (uint64_t)a.N), a.N);
+          st = wroot((int64_t)((jg * (RA * QB)) % (uint64_t)a.N), a.N);
+        }
         V* op = DST + (int64_t)j2 * a.R + c;
 #pragma unroll
         for (int kp = 0; kp < 16; ++kp) {
@@ -475,7 +469,8 @@ __global__ void __launch_bounds__(LT<R>::NT, MINB) lean_pass(const __grid_consta
         const int kb = task * DB + dl;
         V* op = DST + (int64_t)g * F + lane + a.LS * (int64_t)(kb + RA * kq);
         const int64_t step = a.LS * (int64_t)(RA * QB);
-        if (a.cout.x == 1.0 && a.cout.y == 1.0) {  // forward: no conjugation, no scale
+        if (RA == 256 && a.cout.x == 1.0 && a.cout.y == 1.0) {  // forward: no conjugation, no scale
+          // (the odd-factor tiles keep the multiply: a second copy of the stores would spill)
 #pragma unroll
           for (int kp = 0; kp < 16; ++kp) st_hint(op + kp * step, v[P<16>(kp)], pol);
         } else {
@@ -1817,7 +1812,6 @@ static bool plan_pass(Pass& q, bool t1, int ra, int lb, int64_t cols, int64_t N,
   a.cout = make_double2(sc, (!t1 && inverse) ? -sc : sc);
   a.check_finite = t1 && check_finite;
   a.abl = getenv("EFFT_PIPE_ABL") ? atoi(getenv("EFFT_PIPE_ABL")) : 0;
-  a.static_sched = getenv("EFFT_LEAN_STATIC") ? atoi(getenv("EFFT_LEAN_STATIC")) : 0;
   if (cudaFuncSetAttribute((const void*)q.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, q.smem) != cudaSuccess) {
     *err_cuda = 1;
     return false;

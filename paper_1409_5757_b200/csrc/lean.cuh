@@ -45,7 +45,6 @@ struct Args {
   double2 cin;   // (1, +-1): conjugation of the pass input
   double2 cout;  // (s, +-s): conjugation and scale of the pass output
   int32_t check_finite;
-  int32_t static_sched;  // tile kernels: positions c, c + G, ... per CTA instead of the claim counter
   int32_t abl;   // dev ablation bits of the pipelined kernel (EFFT_PIPE_ABL; 0 in production)
 };
 
