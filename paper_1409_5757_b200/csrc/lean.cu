@@ -1106,6 +1106,13 @@ __global__ void __launch_bounds__(pipe::NT, 1) lean_pipe(const __grid_constant__
   }
   // ---------------- compute warps ----------------
   const int q = threadIdx.x / pipe::NC, tid = threadIdx.x % pipe::NC;
+  // T1 B tiles: the tile's four-step twiddle factors, built once per tile in fp64 (as in lean_pair)
+  __shared__ double2 twc_[pipe::NG][T1 ? DB * 8 : 1], twq_[pipe::NG][T1 ? 16 : 1], tws_[pipe::NG][T1 ? DB : 1];
+  __shared__ float2 twj_[pipe::NG][T1 ? DB : 1];
+  double2* const twc = twc_[q];
+  double2* const twq = twq_[q];
+  double2* const tws = tws_[q];
+  float2* const twj = twj_[q];
   pipe::Group* sh = &shs->grp[q];
   unsigned char* const bufs = smraw + q * 2 * pipe::BUF;
   const int cp = tid % 8, r = tid / 8;
@@ -1235,6 +1242,28 @@ __global__ void __launch_bounds__(pipe::NT, 1) lean_pipe(const __grid_constant__
     }
     if (ABL(4)) {
     } else if (isB) {
+      if constexpr (T1) {  // twc[dl][cp], twq[dl][kq], tws[dl], twj[dl]: see lean_pair
+        const uint64_t N = (uint64_t)a.N;
+        const int ks = task & 15;
+        for (int i = tid; i < DB * 8 + 16 + 2 * DB; i += pipe::NC) {
+          int dl2, kind, idx;
+          if (i < DB * 8) {
+            kind = 0, dl2 = i >> 3, idx = i & 7;
+          } else if (i < DB * 8 + 16) {
+            kind = 1, dl2 = (i - DB * 8) / QB, idx = (i - DB * 8) % QB;
+          } else {
+            kind = 2 + ((i - DB * 8 - 16) >= DB), dl2 = (i - DB * 8 - 16) % DB, idx = 0;
+          }
+          const uint64_t jg = (uint64_t)(a.j2off + g * 16 + (task >> 4) * DB + dl2);  // global column
+          const uint64_t m = kind == 0 ? (uint64_t)(2 * idx + 16 * ks) : kind == 1 ? (uint64_t)(256 * idx)
+                             : kind == 2 ? (uint64_t)(256 * QB) : 1ull;
+          const double2 w = wroot((int64_t)((jg * m) % N), a.N);
+          if (kind == 0) twc[i] = w;
+          else if (kind == 1) twq[i - DB * 8] = w;
+          else if (kind == 2) tws[dl2] = w;
+          else twj[dl2] = to_v(w, 0.f);
+        }
+      }
       // the consumed staging lines leave L2 without write-back
 #pragma unroll
       for (int i = cp; i < 16; i += 8) l2_discard(sp + pair_b_line<RB, T1>(task, i / QB, r, i % QB));
@@ -1279,10 +1308,9 @@ __global__ void __launch_bounds__(pipe::NT, 1) lean_pipe(const __grid_constant__
         const int j2 = g * 16 + (task >> 4) * DB + dl;
         const uint32_t c = (uint32_t)(2 * cp + 16 * (task & 15) + 256 * kq);
         // exact integer exponents, fp64 bases and step, fp64 recurrence (see lean_pair)
-        const uint64_t N = (uint64_t)a.N, jg = (uint64_t)(a.j2off + j2);
-        double2 w0 = wroot((int64_t)((jg * c) % N), a.N);
-        const V wj = to_v(wroot((int64_t)(jg % N), a.N), 0.f);
-        const double2 st = wroot((int64_t)((jg * (256 * QB)) % N), a.N);
+        double2 w0 = cmul(twc[dl * 8 + cp], twq[dl * QB + kq]);
+        const V wj = twj[dl];
+        const double2 st = tws[dl];
         if (ABL(2) || ABL(64)) {
         } else if (ABL(128)) {  // timing experiment: the same bytes as 256-byte segments
           const int ks = task & 15;
@@ -1837,9 +1865,10 @@ static bool plan_pass(Pass& q, bool t1, int ra, int lb, int64_t cols, int64_t N,
   const int64_t window = ((q.pipe ? 9 : 4) * (int64_t)q.grid + per - 1) / per;
   // (measured at 2^30: paired 10:16 4.97 / 4.77 ms vs 11:18 5.06 / 4.89 and 13:20 5.44 / 5.13;
   //  wide in-place pass 5:8 4.62 ms vs 6:9 4.69 and 8:12 5.16 -- the ring must stay well inside L2)
-  int64_t lag = window + (getenv("EFFT_LEAN_LAGPLUS") ? atoi(getenv("EFFT_LEAN_LAGPLUS")) : 0);
+  // (pipelined kernel: a finished tile is published ~2 tile periods late -- lag 8, 14 slots at 2^30)
+  int64_t lag = window + (getenv("EFFT_LEAN_LAGPLUS") ? atoi(getenv("EFFT_LEAN_LAGPLUS")) : q.pipe ? 2 : 0);
   if (const char* ev = getenv("EFFT_LEAN_LAG")) lag = atoi(ev);
-  int64_t slots = wide ? lag + 3 : lag + (window + 1) / 2 + 1;  // super-groups (wide: 8 MB slots)
+  int64_t slots = wide ? lag + 3 : q.pipe ? lag + window : lag + (window + 1) / 2 + 1;  // super-groups (wide: 8 MB slots)
   if (const char* ev = getenv("EFFT_LEAN_SLOTS")) slots = atoi(ev);
   if (lag < 1) lag = 1;
   if (lag > G) lag = G;
