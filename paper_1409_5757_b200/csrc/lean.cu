@@ -746,14 +746,16 @@ __global__ void __launch_bounds__(pair::NT, PF ? 3 : 4) lean_pair(const __grid_c
       // ---- A stage 0: 16-point DFTs over t, W_256^(s kt) shared by the pair
       if (a.check_finite) {
         // v * 0 is +-0 for a finite v and NaN for +-Inf / NaN: one FFMA2 per complex value
-        V acc = make_float2(0.f, 0.f);
+        // (four independent accumulators: the chain must not sit on the tile's critical path)
         const V zero = make_float2(0.f, 0.f);
+        V acc[4] = {zero, zero, zero, zero};
 #pragma unroll
         for (int t = 0; t < 16; ++t) {
-          acc = fma2(x[t], zero, acc);
-          acc = fma2(y[t], zero, acc);
+          acc[t & 1] = fma2(x[t], zero, acc[t & 1]);
+          acc[2 + (t & 1)] = fma2(y[t], zero, acc[2 + (t & 1)]);
         }
-        nf |= !(acc.x == 0.f && acc.y == 0.f);
+        const V sum = add2(add2(acc[0], acc[1]), add2(acc[2], acc[3]));
+        nf |= !(sum.x == 0.f && sum.y == 0.f);
       }
       if constexpr (T1) {
         if (a.cin.y != 1.0) {  // inverse: conjugate the input (forward: identity)
@@ -1208,14 +1210,16 @@ __global__ void __launch_bounds__(pipe::NT, 1) lean_pipe(const __grid_constant__
       // ---- A stage 0: 16-point DFTs over t, W_256^(s kt) shared by the pair
       if (a.check_finite) {
         // v * 0 is +-0 for a finite v and NaN for +-Inf / NaN: one FFMA2 per complex value
-        V acc = make_float2(0.f, 0.f);
+        // (four independent accumulators: the chain must not sit on the tile's critical path)
         const V zero = make_float2(0.f, 0.f);
+        V acc[4] = {zero, zero, zero, zero};
 #pragma unroll
         for (int t = 0; t < 16; ++t) {
-          acc = fma2(x[t], zero, acc);
-          acc = fma2(y[t], zero, acc);
+          acc[t & 1] = fma2(x[t], zero, acc[t & 1]);
+          acc[2 + (t & 1)] = fma2(y[t], zero, acc[2 + (t & 1)]);
         }
-        nf |= !(acc.x == 0.f && acc.y == 0.f);
+        const V sum = add2(add2(acc[0], acc[1]), add2(acc[2], acc[3]));
+        nf |= !(sum.x == 0.f && sum.y == 0.f);
       }
       if constexpr (T1) {
         if (a.cin.y != 1.0) {  // inverse: conjugate the input (forward: identity)
@@ -1568,14 +1572,16 @@ __global__ void __launch_bounds__(wide::NT, 2) lean_wide(const __grid_constant__
       // ---- A stage 0: 16-point DFTs over t, W_256^(s kt) shared by the pair
       if (a.check_finite) {
         // v * 0 is +-0 for a finite v and NaN for +-Inf / NaN: one FFMA2 per complex value
-        V acc = make_float2(0.f, 0.f);
+        // (four independent accumulators: the chain must not sit on the tile's critical path)
         const V zero = make_float2(0.f, 0.f);
+        V acc[4] = {zero, zero, zero, zero};
 #pragma unroll
         for (int t = 0; t < 16; ++t) {
-          acc = fma2(x[t], zero, acc);
-          acc = fma2(y[t], zero, acc);
+          acc[t & 1] = fma2(x[t], zero, acc[t & 1]);
+          acc[2 + (t & 1)] = fma2(y[t], zero, acc[2 + (t & 1)]);
         }
-        nf |= !(acc.x == 0.f && acc.y == 0.f);
+        const V sum = add2(add2(acc[0], acc[1]), add2(acc[2], acc[3]));
+        nf |= !(sum.x == 0.f && sum.y == 0.f);
       }
       if constexpr (T1) {
         if (a.cin.y != 1.0) {  // inverse: conjugate the input (forward: identity)
