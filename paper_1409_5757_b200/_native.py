@@ -10,7 +10,8 @@ import os
 
 from . import errors
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libefft_b200.so")
+# EFFT_LIB: another build of the same library (A/B measurements of kernel variants)
+LIB_PATH = os.environ.get("EFFT_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "libefft_b200.so")
 
 EFFT_OK = 0
 EFFT_C64 = 1
